@@ -199,16 +199,16 @@ class Oracle:
             setattr(p, k, v)
         return p
 
-    def memetic(self, n, seed, child_cap=0, **kw):
+    def memetic(self, n, seed, child_cap=None, **kw):
         p = self.params(**kw)
         out = LoRunResult()
-        ce = np.zeros(max(child_cap, 1), dtype=np.int64)
+        ce = np.zeros(max(child_cap or 0, 1), dtype=np.int64)
         rc = self.lib.lo_memetic_tabu(n, C.byref(p), C.c_uint64(seed), None, 0, C.byref(out),
-                                      _p(ce, i64p), child_cap)
+                                      _p(ce, i64p), child_cap or 0)
         if rc != 0:
             raise ValueError("invalid memetic parameters")
         d = _result_dict(out, n)
-        if child_cap:
+        if child_cap is not None:
             d["child_energies"] = ce[:min(child_cap, d["iterations"])].tolist()
         return d
 

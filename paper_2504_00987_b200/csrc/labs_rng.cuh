@@ -1,0 +1,190 @@
+// labs_rng.cuh — warp-uniform random streams for the MTS kernels.
+//
+// Every walker/replica is one warp. All 32 lanes execute each draw together
+// and obtain the same value (warp-uniform control flow), so no shuffles are
+// needed to share a draw; bulk draws (mutation) hand draw i to lane i.
+//
+// Two engines behind one interface:
+//  * MtRng    — reference-RNG mode. std::mt19937_64 with the state in shared
+//               memory and libstdc++ 13's distribution algorithms, restated
+//               so trajectories replay the reference bit for bit
+//               (proj/include/labsolve/rng.hpp:10-28;
+//               /usr/include/c++/13/bits/uniform_int_dist.h:255-281;
+//               /usr/include/c++/13/bits/random.tcc:3346-3381).
+//  * PhiloxRng — production mode. Counter-based Philox4x32-10 keyed by
+//               (seed, stream); draw d is half (d & 1) of block d >> 1. No
+//               per-walker state beyond a 64-bit counter.
+#pragma once
+#include <cstdint>
+
+namespace labsk {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMtN = 312;
+constexpr int kMtM = 156;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+__device__ __forceinline__ uint64_t mt_mix(uint64_t a, uint64_t b, uint64_t c) {
+  // a = mt[i], b = mt[i+1], c = mt[i +/- M]
+  uint64_t x = (a & 0xFFFFFFFF80000000ULL) | (b & 0x7FFFFFFFULL);
+  return c ^ (x >> 1) ^ ((x & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+}
+
+// libstdc++ generate_canonical<double, 53> with one 64-bit draw.
+__device__ __forceinline__ double u01_from_bits(uint64_t x) {
+  double d = __dmul_rn(__ull2double_rn(x), 5.421010862427522170e-20);  // 2^-64
+  if (d >= 1.0) d = 0.99999999999999988898;  // nextafter(1.0, 0.0)
+  return d;
+}
+
+// ---------------------------------------------------------------- MtRng --
+// State layout matches labs_rng_state (include/labs_b200.h): 312 words plus
+// the index of the next output; idx == 312 means "twist before next draw",
+// which is what a freshly seeded engine holds.
+struct MtRng {
+  uint64_t* mt;  // shared memory, 312 words, private to this warp
+  int idx;       // warp-uniform
+
+  // Warp-cooperative twist. Reads of "old" words happen before any lane
+  // overwrites them (syncwarp between the read and write half of a chunk).
+  // Out of line: it runs once per 312 draws and would otherwise be inlined
+  // at every draw site.
+  __device__ __noinline__ void twist() {
+    const int lane = lane_id();
+    // i in [0, 156): inputs mt[i], mt[i+1], mt[i+156], all old.
+#pragma unroll 1
+    for (int base = 0; base < kMtN - kMtM; base += 32) {
+      int i = base + lane;
+      uint64_t v = 0;
+      if (i < kMtN - kMtM) v = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
+      __syncwarp();
+      if (i < kMtN - kMtM) mt[i] = v;
+      __syncwarp();
+    }
+    // i in [156, 311): inputs mt[i], mt[i+1] old, mt[i-156] new.
+#pragma unroll 1
+    for (int base = kMtN - kMtM; base < kMtN - 1; base += 32) {
+      int i = base + lane;
+      uint64_t v = 0;
+      if (i < kMtN - 1) v = mt_mix(mt[i], mt[i + 1], mt[i - (kMtN - kMtM)]);
+      __syncwarp();
+      if (i < kMtN - 1) mt[i] = v;
+      __syncwarp();
+    }
+    if (lane == 0) mt[kMtN - 1] = mt_mix(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
+    __syncwarp();
+    idx = 0;
+  }
+
+  __device__ __forceinline__ uint64_t next() {
+    if (idx >= kMtN) twist();
+    uint64_t y = mt[idx];
+    ++idx;
+    return mt_temper(y);
+  }
+
+  // Bulk: lane i (< count) receives draw i of the next `count` draws, with
+  // count <= 32 and not crossing a twist (callers chunk on room()).
+  __device__ __forceinline__ int room() {
+    if (idx >= kMtN) twist();
+    return kMtN - idx;
+  }
+  __device__ __forceinline__ uint64_t peek_lane(int i) const {
+    return mt_temper(mt[idx + i]);
+  }
+  __device__ __forceinline__ void advance(int count) { idx += count; }
+};
+
+// ------------------------------------------------------------ PhiloxRng --
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0,
+                                              uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c[0]);
+    uint32_t lo0 = 0xD2511F53u * c[0];
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]);
+    uint32_t lo1 = 0xCD9E8D57u * c[2];
+    uint32_t n0 = hi1 ^ c[1] ^ k0;
+    uint32_t n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+struct PhiloxRng {
+  uint32_t k0, k1;   // key = seed
+  uint32_t s0, s1;   // stream (walker / replica id)
+  uint64_t ctr;      // next draw index
+  uint64_t cache;    // upper half of block ctr>>1 when ctr is odd
+
+  __device__ __forceinline__ uint64_t block_half(uint64_t d) const {
+    uint32_t c[4] = {static_cast<uint32_t>(d >> 1),
+                     static_cast<uint32_t>(d >> 33), s0, s1};
+    philox4x32_10(c, k0, k1);
+    return (d & 1ULL) ? (static_cast<uint64_t>(c[3]) << 32 | c[2])
+                      : (static_cast<uint64_t>(c[1]) << 32 | c[0]);
+  }
+  __device__ __forceinline__ uint64_t next() {
+    uint64_t v;
+    if (ctr & 1ULL) {
+      v = cache;
+    } else {
+      uint32_t c[4] = {static_cast<uint32_t>(ctr >> 1),
+                       static_cast<uint32_t>(ctr >> 33), s0, s1};
+      philox4x32_10(c, k0, k1);
+      v = static_cast<uint64_t>(c[1]) << 32 | c[0];
+      cache = static_cast<uint64_t>(c[3]) << 32 | c[2];
+    }
+    ++ctr;
+    return v;
+  }
+  __device__ __forceinline__ int room() { return 1 << 30; }
+  __device__ __forceinline__ uint64_t peek_lane(int i) const {
+    return block_half(ctr + static_cast<uint64_t>(i));
+  }
+  __device__ __forceinline__ void advance(int count) {
+    uint64_t nc = ctr + static_cast<uint64_t>(count);
+    if (nc & 1ULL) cache = block_half(nc);  // keep the odd-index cache valid
+    ctr = nc;
+  }
+};
+
+// ---------------------------------------------------- distributions -------
+// uniform_int_distribution<long long>(lo, hi) over a 64-bit engine: Lemire's
+// nearly-divisionless method on the 128-bit product; at least one draw.
+template <class R>
+__device__ __forceinline__ long long uniform_int(R& rng, long long lo,
+                                                 long long hi) {
+  const uint64_t range =
+      static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo) + 1ULL;
+  uint64_t x = rng.next();
+  uint64_t low = x * range;
+  if (low < range) {
+    const uint64_t thr = (0ULL - range) % range;
+    while (low < thr) {
+      x = rng.next();
+      low = x * range;
+    }
+  }
+  return static_cast<long long>(static_cast<uint64_t>(lo) + __umul64hi(x, range));
+}
+
+template <class R>
+__device__ __forceinline__ double uniform01(R& rng) {
+  return u01_from_bits(rng.next());
+}
+
+}  // namespace labsk
