@@ -1,0 +1,337 @@
+#!/usr/bin/env python3
+"""bench.py — tabu flip-evaluations/s of the B200 memetic tabu search (LABS).
+
+Workload (BASELINE.json configs[1]): LABS N=64 on one B200, one warp per
+replica/walker, replicas = device resident capacity, reference MemeticParams
+(K=100, p_comb=0.9, p_mutate=1/N, tenure 0.10/0.12), target unreachable so
+every replica keeps searching. A "step" is one labs_solver_run launch: every
+replica advances its memetic_tabu loop for `--epoch-ms` of device time
+(population, RNG and best stay resident in HBM between steps). One
+flip-evaluation = the dE of one candidate flip in one tabu iteration (N per
+iteration).
+
+  value   flip-evals/s, device-resident, CUDA events on the solver stream,
+          L2 flushed (256 MiB write) between timed steps, max over ranks.
+  e2e     same metric through the reference-facing C-ABI call
+          labs_run_replicas (host buffers in and out, allocation, seeding,
+          population init and result copy-back inside the timed region).
+  cpu_baseline   the reference's own tabu_search (oracle/_ref, unmodified
+          sources) on every host core for --cpu-seconds.
+  tts     time to the best-known energy (N=64 -> 208) on this GPU.
+
+--impl reference runs the reference's multithreaded CPU tabu_search on the
+host cores with the same metric (rank 0 only under torchrun).
+Multi-GPU (torchrun, one rank per GPU): each rank runs its own replica set
+(global replica ids rank*R + r, seeds base + id); weak scaling, no data-path
+collective. The island model (elite allgather) is exercised by --islands.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+OPS_PER_FLIP_EVAL = 13  # int32 ops per candidate per tabu iteration
+TARGETS = {32: 64, 64: 208}  # Packebusch & Mertens 2016 optima
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--epoch-ms", type=float, default=100.0)
+    ap.add_argument("--rng", choices=["mt19937_64", "philox"], default="mt19937_64")
+    ap.add_argument("--replicas", type=int, default=0, help="0 = resident capacity")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--tts-seeds", type=int, default=3)
+    ap.add_argument("--tts-limit", type=float, default=30.0)
+    ap.add_argument("--islands", type=int, default=0,
+                    help="elite exchange every this many steps (0 = off)")
+    ap.add_argument("--quick", action="store_true", help="skip cpu baseline and TTS")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_throughput(n: int, seconds: float):
+    """The reference's tabu_search on every host core (or the oracle port)."""
+    from oracle.pyoracle import Oracle, Reference, reference_available
+    threads = os.cpu_count() or 1
+    if reference_available():
+        it, walks, el = Reference().tabu_throughput(n, threads, seconds)
+        kind = "reference"
+    else:
+        it, walks, el = Oracle().tabu_throughput(n, threads, seconds)
+        kind = "port"
+    return {"value": it * n / el, "unit": "flip-evals/s", "cores": threads, "kind": kind,
+            "sample": f"{walks} tabu_search walks from Sequence::random({n}), "
+                      f"{threads} threads x {seconds:.0f} s, TabuParams{{0.10,0.12}}"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    per_step = max(1.0, min(5.0, 60.0 / max(args.steps + args.warmup, 1)))
+    for _ in range(args.warmup):
+        cpu_reference_throughput(args.n, min(per_step, 1.0))
+    vals = []
+    total_evals, total_t = 0.0, 0.0
+    for _ in range(args.steps):
+        r = cpu_reference_throughput(args.n, per_step)
+        vals.append(r)
+        total_evals += r["value"] * per_step
+        total_t += per_step
+    v = total_evals / total_t
+    line = {"metric": "tabu flip-evals/sec", "value": v, "unit": "flip-evals/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"LABS N={args.n} tabu_search throughput, reference CPU",
+                       "n": args.n},
+            "impl": "reference",
+            "cpu_baseline": {**vals[-1], "value": v},
+            "e2e": {"value": v, "unit": "flip-evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2504_00987_b200 import capi
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = capi.Context(local)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    n = args.n
+    rng_kind = capi.RNG_PHILOX if args.rng == "philox" else capi.RNG_MT19937_64
+    cap = capi.Solver.capacity(ctx, n, rng_kind)
+    R = args.replicas or cap
+    params = capi.memetic_params(target_energy=0, rng_kind=rng_kind)
+    solver = capi.Solver(ctx, n, R, base_seed=1000, replica_offset=rank * R, params=params)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
+    epoch_s = args.epoch_ms / 1e3
+
+    # islands: k elites per GPU, gathered over NCCL between steps
+    k_el = 16
+    nw = (n + 63) // 64
+    el_w = torch.zeros(k_el * nw, dtype=torch.int64, device=f"cuda:{local}")
+    el_e = torch.zeros(k_el, dtype=torch.int64, device=f"cuda:{local}")
+    all_w = torch.zeros(world * k_el * nw, dtype=torch.int64, device=f"cuda:{local}")
+    all_e = torch.zeros(world * k_el, dtype=torch.int64, device=f"cuda:{local}")
+
+    def exchange(step):
+        solver.export_elites(k_el, el_w.data_ptr(), el_e.data_ptr())
+        with torch.cuda.stream(ext):
+            if world > 1:
+                dist.all_gather_into_tensor(all_w, el_w)
+                dist.all_gather_into_tensor(all_e, el_e)
+            else:
+                all_w.copy_(el_w)
+                all_e.copy_(el_e)
+        solver.import_elites(world * k_el, all_w.data_ptr(), all_e.data_ptr(), rotation=step)
+
+    for _ in range(args.warmup):
+        solver.run(epoch_seconds=epoch_s, race=False)
+    ctx.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_before, m_before = solver.counters()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    launches = 0
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            with torch.cuda.stream(ext):
+                flush.fill_(k)  # evict L2 between timed steps (not timed)
+                starts[k].record(ext)
+            solver.run(epoch_seconds=epoch_s, race=False)
+            launches += 1
+            with torch.cuda.stream(ext):
+                ends[k].record(ext)
+            if args.islands and (k + 1) % args.islands == 0:
+                exchange(k)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_after, m_after = solver.counters()
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    evals_local = float(t_after - t_before) * n
+    if world > 1:
+        tt = torch.tensor([evals_local, dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+        ev = tt[:1].clone()
+        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        mx = tt[1:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        evals_total, time_ms = float(ev.item()), float(mx.item())
+    else:
+        evals_total, time_ms = evals_local, dev_ms
+    value = evals_total / (time_ms / 1e3)
+    per_gpu = value / world
+
+    # roofline: the memetic kernel is the step (one launch per step)
+    peak_gops = ctx.int_peak_gops()
+    achieved_gops = per_gpu * OPS_PER_FLIP_EVAL / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"k_memetic_n{n}_per_launch_bytes")
+        except Exception:
+            traffic = None
+
+    # e2e through the reference-facing C-ABI call with host buffers
+    e2e_iters = 400
+    e2e_params = capi.memetic_params(target_energy=0, max_iterations=e2e_iters,
+                                     rng_kind=rng_kind)
+    ctx.run_replicas(n, R, 7, e2e_params)  # warm
+    t0 = time.perf_counter()
+    best, per = ctx.run_replicas(n, R, 1000 + rank * R, e2e_params)
+    e2e_t = time.perf_counter() - t0
+    e2e_evals = sum(p["tabu_iterations"] for p in per) * n
+    e2e_value = e2e_evals / e2e_t
+    if world > 1:
+        t = torch.tensor([e2e_evals, e2e_t], dtype=torch.float64, device=f"cuda:{local}")
+        a = t[:1].clone()
+        dist.all_reduce(a)
+        b = t[1:].clone()
+        dist.all_reduce(b, op=dist.ReduceOp.MAX)
+        e2e_value = float(a.item()) / float(b.item())
+    d2h = R * capi.C.sizeof(capi.RunResult) + R * 4 * 3
+    h2d = capi.C.sizeof(capi.MemeticParams)
+
+    line = {
+        "metric": "tabu flip-evals/sec", "value": value, "unit": "flip-evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": time_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"LABS N={n} memetic tabu search, {R} replicas/GPU "
+                               f"(one warp each), K=100, {args.rng} RNG, "
+                               f"{args.epoch_ms:.0f} ms device epochs",
+                   "n": n, "replicas_per_gpu": R, "population": 100,
+                   "rng": args.rng, "epoch_ms": args.epoch_ms,
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "islands": args.islands},
+        "per_gpu": per_gpu,
+        "memetic_iterations": m_after - m_before,
+        "gpu_launches": launches,
+        "roofline": {"bound": "int32", "achieved": achieved_gops, "peak": peak_gops,
+                     "unit": "Gop/s", "frac": achieved_gops / peak_gops, "traffic": traffic,
+                     "ops_per_flip_eval": OPS_PER_FLIP_EVAL,
+                     "peak_source": "measured on this device (labs_bench_int_peak)",
+                     "lag_term_equiv_frac": per_gpu * (n - 1) / (peak_gops * 1e9)},
+        "e2e": {"value": e2e_value, "unit": "flip-evals/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "call": f"labs_run_replicas(n={n}, replicas={R}, max_iterations={e2e_iters})"},
+        "clocks": clocks.summary(),
+    }
+    solver.close()
+
+    if rank == 0 and world == 1 and not args.quick:
+        line["cpu_baseline"] = cpu_reference_throughput(n, args.cpu_seconds)
+        if n in TARGETS and args.tts_seeds > 0:
+            line["tts"] = time_to_target(ctx, capi, n, TARGETS[n], R, rng_kind, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def time_to_target(ctx, capi, n, target, R, rng_kind, args):
+    """Wall time from solver creation to the first replica at the target."""
+    times, censored = [], 0
+    for s in range(args.tts_seeds):
+        params = capi.memetic_params(target_energy=target, rng_kind=rng_kind,
+                                     max_seconds=args.tts_limit)
+        t0 = time.perf_counter()
+        sv = capi.Solver(ctx, n, R, base_seed=1000 * (s + 1), params=params)
+        sv.run(race=True)
+        st = sv.status()
+        dt = time.perf_counter() - t0
+        if st["best_energy"] <= target:
+            times.append(dt)
+        else:
+            censored += 1
+        sv.close()
+    return {"n": n, "target": target, "seeds": args.tts_seeds, "censored": censored,
+            "limit_s": args.tts_limit, "times_s": times,
+            "median_s": statistics.median(times) if times else None,
+            "paper_a100_fit_s": 8.23e-8 * 1.313 ** n}
+
+
+if __name__ == "__main__":
+    main()

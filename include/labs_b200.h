@@ -54,6 +54,13 @@ extern "C" {
 #define LABS_TIE_REFERENCE 0 /* uniform draw among ties (reference) */
 #define LABS_TIE_LOWEST 1    /* deterministic: lowest position, no draw */
 
+#define LABS_CROSSOVER_UNIFORM 0   /* one bits64() mask per word (reference) */
+#define LABS_CROSSOVER_ONE_POINT 1 /* cut = uniform_int(1, n-1) */
+
+#define LABS_REPLACE_RANDOM 0 /* victim = uniform_int(0, K-1) (reference) */
+#define LABS_REPLACE_WORST 1  /* elite-preserving: child replaces the worst
+                                 member only if strictly better */
+
 typedef struct labs_ctx labs_ctx;
 
 /* mt19937_64 engine state: 312 words + next-output index (312 = fresh). */
@@ -92,6 +99,8 @@ typedef struct {
   double max_seconds;
   int64_t max_iterations;
   labs_tabu_params tabu;
+  int32_t crossover;   /* LABS_CROSSOVER_*; reference: UNIFORM */
+  int32_t replacement; /* LABS_REPLACE_*; reference: RANDOM */
 } labs_memetic_params;
 
 /* RunResult (proj/include/labsolve/memetic.hpp:26-35). */
@@ -104,6 +113,7 @@ typedef struct {
   uint64_t seed;
   int32_t replica_id;
   int32_t reached_target;
+  int64_t tabu_iterations; /* extension: tabu iterations this replica ran */
 } labs_run_result;
 
 /* MemeticIterRecord (proj/include/labsolve/memetic.hpp:37-41). */
@@ -210,6 +220,57 @@ int labs_run_replicas(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
                       labs_run_result* per_replica,
                       labs_memetic_record* traces, int64_t trace_cap,
                       int64_t* trace_len);
+
+/* ------------------------------------------- solver (epoch-driven K4) ---- */
+/* Device-resident replica set for long runs, throughput measurement and the
+ * island model: population, energies, best and RNG state of every replica
+ * stay in HBM between labs_solver_run calls, so cutting a run into epochs
+ * never changes a replica's trajectory. Replica r (global id
+ * replica_offset + r) is seeded base_seed + replica_offset + r.
+ * trace_cap > 0 keeps up to trace_cap memetic records per replica. */
+typedef struct labs_solver labs_solver;
+
+int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
+                       int64_t replica_offset,
+                       const labs_memetic_params* params, int64_t trace_cap,
+                       labs_solver** out);
+int labs_solver_destroy(labs_solver* s);
+/* Replicas resident at once for (n, rng_kind) on this device. */
+int labs_solver_capacity(labs_ctx* ctx, int n, int rng_kind);
+/* One launch (asynchronous on the context stream). Each replica stops at
+ * its reference exit conditions, or after epoch_iterations more memetic
+ * iterations (< 0: no limit), or when epoch_seconds have elapsed since the
+ * replica resumed (< 0: no limit; checked between memetic iterations).
+ * race != 0: a replica reaching the target raises the stop flag. */
+int labs_solver_run(labs_solver* s, int64_t epoch_iterations,
+                    double epoch_seconds, int race);
+/* Set the device stop flag (replicas see it at their next loop check). */
+int labs_solver_request_stop(labs_solver* s);
+/* Synchronizing queries. */
+int labs_solver_status(labs_solver* s, int32_t* running, int64_t* best_energy,
+                       int32_t* best_replica);
+int labs_solver_counters(labs_solver* s, uint64_t* tabu_iterations,
+                         int64_t* memetic_iterations);
+/* Per-replica RunResults (replicas entries), optional traces
+ * (replicas x trace_cap) with lengths, optional publish order. */
+int labs_solver_results(labs_solver* s, labs_run_result* per_replica,
+                        labs_memetic_record* traces, int64_t* trace_len,
+                        int32_t* publish_order);
+/* Island model (device pointers, asynchronous). export: the k best replica
+ * bests (k x ceil(n/64) words, k energies), best first. import: replica r
+ * offers elite (r + rotation) % count to its population, replacing its worst
+ * member if the elite is strictly better. */
+int labs_solver_export_elites(labs_solver* s, int k, uint64_t* d_words,
+                              int64_t* d_energies);
+int labs_solver_import_elites(labs_solver* s, int count,
+                              const uint64_t* d_words,
+                              const int64_t* d_energies, int rotation);
+
+/* ------------------------------------------------------- diagnostics --- */
+/* Measured INT32 lane-instruction rate of this device (IMAD on the FMA pipe
+ * alongside IADD3/LOP3 on the ALU pipe), in Gop/s: the roofline denominator
+ * bench.py reports the integer-bound walker against. */
+int labs_bench_int_peak(labs_ctx* ctx, double* gops);
 
 #ifdef __cplusplus
 }

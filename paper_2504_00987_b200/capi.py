@@ -42,8 +42,15 @@ EXPORTS = [
     "labs_ctx_sm_count", "labs_ctx_synchronize", "labs_max_n", "labs_rng_seed",
     "labs_build_state", "labs_flip_trace", "labs_scan", "labs_tabu_walks",
     "labs_tabu_walks_device", "labs_rng_seed_device", "labs_memetic",
-    "labs_run_replicas",
+    "labs_run_replicas", "labs_solver_create", "labs_solver_destroy", "labs_solver_capacity",
+    "labs_solver_run", "labs_solver_request_stop", "labs_solver_status", "labs_solver_counters",
+    "labs_solver_results", "labs_solver_export_elites", "labs_solver_import_elites",
+    "labs_bench_int_peak",
 ]
+CROSSOVER_UNIFORM = 0
+CROSSOVER_ONE_POINT = 1
+REPLACE_RANDOM = 0
+REPLACE_WORST = 1
 
 
 class LabsCudaError(RuntimeError):
@@ -69,14 +76,16 @@ class MemeticParams(C.Structure):
     _fields_ = [("population_size", C.c_int32), ("rng_kind", C.c_int32),
                 ("p_comb", C.c_double), ("p_mutate", C.c_double),
                 ("target_energy", C.c_int64), ("max_seconds", C.c_double),
-                ("max_iterations", C.c_int64), ("tabu", TabuParams)]
+                ("max_iterations", C.c_int64), ("tabu", TabuParams),
+                ("crossover", C.c_int32), ("replacement", C.c_int32)]
 
 
 class RunResult(C.Structure):
     _fields_ = [("best", C.c_uint64 * LABS_MAX_WORDS), ("best_energy", C.c_int64),
                 ("merit", C.c_double), ("iterations", C.c_int64),
                 ("wall_seconds", C.c_double), ("seed", C.c_uint64),
-                ("replica_id", C.c_int32), ("reached_target", C.c_int32)]
+                ("replica_id", C.c_int32), ("reached_target", C.c_int32),
+                ("tabu_iterations", C.c_int64)]
 
 
 class MemeticRecord(C.Structure):
@@ -92,13 +101,15 @@ def tabu_params(min_tabu_factor=0.10, max_tabu_factor=0.12, tie_rule=TIE_REFEREN
 
 def memetic_params(population_size=100, p_comb=0.9, p_mutate=None, target_energy=0,
                    max_seconds=None, max_iterations=None, rng_kind=RNG_MT19937_64,
+                   crossover=CROSSOVER_UNIFORM, replacement=REPLACE_RANDOM,
                    **tabu_kw) -> MemeticParams:
-    """MemeticParams defaults (proj/include/labsolve/memetic.hpp:15-24)."""
+    """MemeticParams defaults (proj/include/labsolve/memetic.hpp:15-24); the
+    reference policies are the defaults of every switch."""
     return MemeticParams(population_size, rng_kind, p_comb,
                          -1.0 if p_mutate is None else float(p_mutate), int(target_energy),
                          -1.0 if max_seconds is None else float(max_seconds),
                          -1 if max_iterations is None else int(max_iterations),
-                         tabu_params(**tabu_kw))
+                         tabu_params(**tabu_kw), crossover, replacement)
 
 
 u64p = C.POINTER(C.c_uint64)
@@ -155,6 +166,21 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                     C.POINTER(MemeticParams), C.POINTER(RunResult),
                                     C.POINTER(RunResult), C.POINTER(MemeticRecord), C.c_int64,
                                     i64p]
+    L.labs_solver_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_int64,
+                                     C.POINTER(MemeticParams), C.c_int64,
+                                     C.POINTER(C.c_void_p)]
+    L.labs_solver_destroy.argtypes = [C.c_void_p]
+    L.labs_solver_capacity.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.labs_solver_run.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.c_int]
+    L.labs_solver_request_stop.argtypes = [C.c_void_p]
+    L.labs_solver_status.argtypes = [C.c_void_p, i32p, i64p, i32p]
+    L.labs_solver_counters.argtypes = [C.c_void_p, u64p, i64p]
+    L.labs_solver_results.argtypes = [C.c_void_p, C.POINTER(RunResult),
+                                      C.POINTER(MemeticRecord), i64p, i32p]
+    L.labs_solver_export_elites.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    L.labs_solver_import_elites.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_int]
+    L.labs_bench_int_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -202,7 +228,7 @@ def _result(r: RunResult, n: int) -> dict:
             "best_energy": int(r.best_energy), "merit": float(r.merit),
             "iterations": int(r.iterations), "wall_seconds": float(r.wall_seconds),
             "seed": int(r.seed), "replica_id": int(r.replica_id),
-            "reached_target": bool(r.reached_target)}
+            "reached_target": bool(r.reached_target), "tabu_iterations": int(r.tabu_iterations)}
 
 
 class Context:
@@ -236,6 +262,12 @@ class Context:
 
     def synchronize(self):
         _check(self.L.labs_ctx_synchronize(self.h))
+
+    def int_peak_gops(self) -> float:
+        """Measured INT32 lane-instruction rate (roofline denominator)."""
+        g = C.c_double(0)
+        _check(self.L.labs_bench_int_peak(self.h, C.byref(g)))
+        return float(g.value)
 
     # -- K1 ---------------------------------------------------------------
     def build_state(self, n: int, words, neighbors: bool = True):
@@ -360,3 +392,77 @@ class Context:
                                      int(tr[r * trace_cap + i].child_energy))
                                     for i in range(int(tl[r]))]
         return res, reps
+
+
+class Solver:
+    """Device-resident replica set (labs_solver_*): epochs, counters, island
+    exchange. Replica r has global id replica_offset + r and seed
+    base_seed + replica_offset + r."""
+
+    def __init__(self, ctx: Context, n: int, replicas: int, base_seed: int,
+                 params: MemeticParams | None = None, replica_offset: int = 0,
+                 trace_cap: int = 0):
+        self.ctx, self.L = ctx, ctx.L
+        self.n, self.replicas, self.trace_cap = n, replicas, trace_cap
+        self.params = params or memetic_params()
+        h = C.c_void_p()
+        _check(self.L.labs_solver_create(ctx.h, n, replicas, C.c_uint64(base_seed),
+                                         replica_offset, C.byref(self.params), trace_cap,
+                                         C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.labs_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def capacity(ctx: Context, n: int, rng_kind: int = RNG_MT19937_64) -> int:
+        return int(ctx.L.labs_solver_capacity(ctx.h, n, rng_kind))
+
+    def run(self, epoch_iterations: int = -1, epoch_seconds: float = -1.0, race: bool = True):
+        _check(self.L.labs_solver_run(self.h, epoch_iterations, epoch_seconds, 1 if race else 0))
+
+    def request_stop(self):
+        _check(self.L.labs_solver_request_stop(self.h))
+
+    def status(self):
+        run, be, br = C.c_int32(0), C.c_int64(0), C.c_int32(0)
+        _check(self.L.labs_solver_status(self.h, C.byref(run), C.byref(be), C.byref(br)))
+        return {"running": run.value, "best_energy": be.value, "best_replica": br.value}
+
+    def counters(self):
+        t, m = C.c_uint64(0), C.c_int64(0)
+        _check(self.L.labs_solver_counters(self.h, C.byref(t), C.byref(m)))
+        return int(t.value), int(m.value)
+
+    def results(self):
+        per = (RunResult * self.replicas)()
+        order = np.zeros(self.replicas, dtype=np.int32)
+        tr = (MemeticRecord * (self.replicas * self.trace_cap))() if self.trace_cap else None
+        tl = np.zeros(self.replicas, dtype=np.int64)
+        _check(self.L.labs_solver_results(self.h, per, tr, _ptr(tl, i64p) if self.trace_cap
+                                          else None, _ptr(order, i32p)))
+        reps = [_result(per[i], self.n) for i in range(self.replicas)]
+        for i, r in enumerate(reps):
+            r["publish_order"] = int(order[i])
+            if self.trace_cap:
+                r["trace"] = [(int(tr[i * self.trace_cap + j].iteration),
+                               bool(tr[i * self.trace_cap + j].stop_seen),
+                               int(tr[i * self.trace_cap + j].child_energy))
+                              for j in range(int(tl[i]))]
+        return reps
+
+    def export_elites(self, k: int, d_words: int, d_energies: int):
+        _check(self.L.labs_solver_export_elites(self.h, k, C.c_void_p(d_words),
+                                                C.c_void_p(d_energies)))
+
+    def import_elites(self, count: int, d_words: int, d_energies: int, rotation: int = 0):
+        _check(self.L.labs_solver_import_elites(self.h, count, C.c_void_p(d_words),
+                                                C.c_void_p(d_energies), rotation))

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_memetic(Memet
       PhiloxRng rng;
       rng.k0 = static_cast<uint32_t>(A.base_seed);
       rng.k1 = static_cast<uint32_t>(A.base_seed >> 32);
-      rng.s0 = static_cast<uint32_t>(r);
+      rng.s0 = static_cast<uint32_t>(A.replica_offset + r);
       rng.s1 = 0x4D454D45u;  // "MEME"
       rng.ctr = A.ctr[r];
       rng.cache = (rng.ctr & 1ULL) ? rng.block_half(rng.ctr) : 0ULL;
@@ -296,6 +297,100 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_memetic(Memet
     }
     __syncwarp();
   }
+}
+
+
+// ---------------------------------------------------- island exchange ----
+// Top-k replica bests, best first: k rounds of a block-wide argmin over the
+// packed key (E << 32 | replica); taken replicas are masked in `taken`.
+__global__ void k_export_elites(int replicas, int nw, int k, const int32_t* bestE,
+                                const uint64_t* best, int32_t* taken, uint64_t* out_words,
+                                int64_t* out_e) {
+  __shared__ unsigned long long red[32];
+  for (int i = threadIdx.x; i < replicas; i += blockDim.x) taken[i] = 0;
+  __syncthreads();
+  for (int sel = 0; sel < k; ++sel) {
+    unsigned long long key = ~0ULL;
+    for (int i = threadIdx.x; i < replicas; i += blockDim.x)
+      if (!taken[i]) {
+        const unsigned long long v =
+            (static_cast<unsigned long long>(static_cast<uint32_t>(bestE[i])) << 32) | i;
+        key = v < key ? v : key;
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(kFull, key, o);
+      key = x < key ? x : key;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      unsigned long long v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : ~0ULL;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(kFull, v, o);
+        v = x < v ? x : v;
+      }
+      if (threadIdx.x == 0) {
+        const int r = static_cast<int>(v & 0xffffffffULL);
+        if (v != ~0ULL) {
+          taken[r] = 1;
+          out_e[sel] = static_cast<int64_t>(v >> 32);
+          for (int w = 0; w < nw; ++w) out_words[static_cast<size_t>(sel) * nw + w] =
+              best[static_cast<size_t>(r) * nw + w];
+        } else {
+          out_e[sel] = INT_MAX;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Replica r offers elite (r + rotation) % count: it replaces the worst
+// population member when strictly better. One warp per replica.
+__global__ void k_import_elites(int replicas, int nw, int K, int count, int rotation,
+                                const uint64_t* words, const int64_t* energies,
+                                uint64_t* pop, int32_t* popE, const int32_t* status) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= replicas || status[r] != kRunning) return;
+  const int e = (r + rotation) % count;
+  const int64_t ee = energies[e];
+  int32_t* pe = popE + static_cast<size_t>(r) * K;
+  const int victim = worst_member(pe, K);
+  if (ee < pe[victim]) {
+    if (lane_id() < nw)
+      pop[(static_cast<size_t>(r) * K + victim) * nw + lane_id()] =
+          words[static_cast<size_t>(e) * nw + lane_id()];
+    if (lane_id() == 0) pe[victim] = static_cast<int32_t>(ee);
+  }
+}
+
+
+// ------------------------------------------------ INT32 issue-rate probe --
+// Roofline denominator for the integer-bound walker: 8 independent chains per
+// thread, 4 on the FMA pipe (IMAD) and 4 on the ALU pipe (IADD3/LOP3), so
+// both integer pipes issue every cycle. One "op" = one lane-instruction.
+__global__ void __launch_bounds__(256) k_int_peak(int iters, int seed, int* sink) {
+  int a0 = threadIdx.x ^ seed, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  int b0 = blockIdx.x ^ seed, b1 = b0 + 5, b2 = b0 + 6, b3 = b0 + 7;
+  const int m = seed | 1;
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = a0 * m + b3;
+      a1 = a1 * m + b2;
+      a2 = a2 * m + b1;
+      a3 = a3 * m + b0;
+      b0 = b0 + a1 + u;
+      b1 = b1 ^ a2 ^ u;
+      b2 = b2 + a3 + 3;
+      b3 = b3 ^ a0 ^ 9;
+    }
+  }
+  const int v = a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3;
+  if (v == 0x7fffffff) sink[0] = v;  // keep the chains alive
 }
 
 }  // namespace labsk
@@ -729,13 +824,9 @@ int labs_rng_seed_device(labs_ctx* ctx, int count, uint64_t base_seed, labs_rng_
 
 }  // extern "C"
 
+
 // ------------------------------------------------------- memetic (K4) ----
 namespace {
-
-struct MemeticRun {
-  DBuf pop, popE, best, bestE, iters, status, init, t0, tend, order, counter, mt, ctr, stop,
-      tabu_iters, trace, trace_len;
-};
 
 int check_memetic(int n, const labs_memetic_params* p) {
   if (int rc = check_n(n)) return rc;
@@ -748,149 +839,279 @@ int check_memetic(int n, const labs_memetic_params* p) {
     return fail(LABS_ERR_INVALID_ARGUMENT, "mutation probability must be in (0, 1]");
   if (p->rng_kind != LABS_RNG_MT19937_64 && p->rng_kind != LABS_RNG_PHILOX)
     return fail(LABS_ERR_INVALID_ARGUMENT, "unknown rng kind");
+  if (p->crossover != LABS_CROSSOVER_UNIFORM && p->crossover != LABS_CROSSOVER_ONE_POINT)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "unknown crossover");
+  if (p->replacement != LABS_REPLACE_RANDOM && p->replacement != LABS_REPLACE_WORST)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "unknown replacement policy");
   return check_tabu(&p->tabu);
 }
 
-// Runs `replicas` memetic replicas to completion. host_stop, when given, is
-// polled between epochs and forwarded to the device stop flag.
-int run_memetic(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
-                const labs_memetic_params* p, const volatile int32_t* host_stop, int race,
-                labs_run_result* per_replica, labs_memetic_record* traces, int64_t trace_cap,
-                int64_t* trace_len, std::vector<int32_t>* order_out) {
+template <int NS, bool MT>
+int launch_memetic(labs_ctx* ctx, const MemeticArgs& A) {
+  const size_t smem = kWarps * slot_bytes<NS, MT>();
+  auto kern = k_memetic<NS, MT>;
+  if (int r = prep(kern, smem)) return r;
+  int grid = 0;
+  if (int r = grid_for(ctx, kern, smem, A.replicas, &grid)) return r;
+  kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
+  LABS_CUDA(cudaGetLastError());
+  return LABS_OK;
+}
+
+}  // namespace
+
+// Device-resident replica set (include/labs_b200.h: labs_solver_*).
+struct labs_solver {
+  labs_ctx* ctx = nullptr;
+  int n = 0, nw = 0, R = 0, K = 0;
+  uint64_t base_seed = 0;
+  int64_t offset = 0;
+  labs_memetic_params p{};
+  bool mt = true;
+  int64_t trace_cap = 0;
+  DBuf pop, popE, best, bestE, iters, status, init, t0, tend, order, counter, rng, ctr, stop,
+      tabu_total, tabu_rep, trace, trace_len, taken;
+  MemeticArgs A{};
+};
+
+extern "C" {
+
+int labs_solver_capacity(labs_ctx* ctx, int n, int rng_kind) {
+  if (!ctx || check_n(n)) return 0;
+  int out = 0;
+  cudaSetDevice(ctx->device);
+  dispatch(n, [&](auto ns) -> int {
+    constexpr int NS = decltype(ns)::value;
+    int per_sm = 0;
+    if (rng_kind == LABS_RNG_MT19937_64)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, true>, 32 * kWarps,
+                                                    kWarps * slot_bytes<NS, true>());
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, false>, 32 * kWarps,
+                                                    kWarps * slot_bytes<NS, false>());
+    out = per_sm * ctx->sm_count * kWarps;
+    return LABS_OK;
+  });
+  return out;
+}
+
+int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
+                       int64_t replica_offset, const labs_memetic_params* params,
+                       int64_t trace_cap, labs_solver** out) {
+  if (!ctx || !out) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (replicas < 1) return fail(LABS_ERR_INVALID_ARGUMENT, "replicas must be >= 1");
+  if (int rc = check_memetic(n, params)) return rc;
+  if (trace_cap < 0 || replica_offset < 0)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "bad trace capacity or replica offset");
   LABS_CUDA(cudaSetDevice(ctx->device));
-  const int nw = nw_of(n), K = p->population_size;
-  const bool mt = p->rng_kind == LABS_RNG_MT19937_64;
-  MemeticRun b;
-  LABS_ALLOC(b.pop, sizeof(uint64_t) * replicas * K * nw);
-  LABS_ALLOC(b.popE, sizeof(int32_t) * replicas * K);
-  LABS_ALLOC(b.best, sizeof(uint64_t) * replicas * nw);
-  LABS_ALLOC(b.bestE, sizeof(int32_t) * replicas);
-  LABS_ALLOC(b.iters, sizeof(int64_t) * replicas);
-  LABS_ALLOC(b.status, sizeof(int32_t) * replicas);
-  LABS_ALLOC(b.init, sizeof(int32_t) * replicas);
-  LABS_ALLOC(b.t0, sizeof(int64_t) * replicas);
-  LABS_ALLOC(b.tend, sizeof(int64_t) * replicas);
-  LABS_ALLOC(b.order, sizeof(int32_t) * replicas);
-  LABS_ALLOC(b.counter, sizeof(int32_t));
-  LABS_ALLOC(b.stop, sizeof(int32_t));
-  if (mt) LABS_ALLOC(b.mt, sizeof(labs_rng_state) * replicas);
-  else LABS_ALLOC(b.ctr, sizeof(uint64_t) * replicas);
-  if (traces) {
-    LABS_ALLOC(b.trace, sizeof(int64_t) * 3 * replicas * std::max<int64_t>(trace_cap, 1));
-    LABS_ALLOC(b.trace_len, sizeof(int64_t) * replicas);
+  auto* s = new labs_solver;
+  std::unique_ptr<labs_solver> guard(s);
+  s->ctx = ctx;
+  s->n = n;
+  s->nw = nw_of(n);
+  s->R = replicas;
+  s->K = params->population_size;
+  s->base_seed = base_seed;
+  s->offset = replica_offset;
+  s->p = *params;
+  s->mt = params->rng_kind == LABS_RNG_MT19937_64;
+  s->trace_cap = trace_cap;
+  const size_t R = replicas, K = s->K, nw = s->nw;
+  LABS_ALLOC(s->pop, sizeof(uint64_t) * R * K * nw);
+  LABS_ALLOC(s->popE, sizeof(int32_t) * R * K);
+  LABS_ALLOC(s->best, sizeof(uint64_t) * R * nw);
+  LABS_ALLOC(s->bestE, sizeof(int32_t) * R);
+  LABS_ALLOC(s->iters, sizeof(int64_t) * R);
+  LABS_ALLOC(s->status, sizeof(int32_t) * R);
+  LABS_ALLOC(s->init, sizeof(int32_t) * R);
+  LABS_ALLOC(s->t0, sizeof(int64_t) * R);
+  LABS_ALLOC(s->tend, sizeof(int64_t) * R);
+  LABS_ALLOC(s->order, sizeof(int32_t) * R);
+  LABS_ALLOC(s->counter, sizeof(int32_t));
+  LABS_ALLOC(s->stop, sizeof(int32_t));
+  LABS_ALLOC(s->tabu_total, sizeof(unsigned long long));
+  LABS_ALLOC(s->tabu_rep, sizeof(int64_t) * R);
+  LABS_ALLOC(s->taken, sizeof(int32_t) * R);
+  if (s->mt) LABS_ALLOC(s->rng, sizeof(labs_rng_state) * R);
+  else LABS_ALLOC(s->ctr, sizeof(uint64_t) * R);
+  if (trace_cap) {
+    LABS_ALLOC(s->trace, sizeof(int64_t) * 3 * R * trace_cap);
+    LABS_ALLOC(s->trace_len, sizeof(int64_t) * R);
   }
-  LABS_CUDA(cudaMemsetAsync(b.init.p, 0, sizeof(int32_t) * replicas, ctx->stream));
-  LABS_CUDA(cudaMemsetAsync(b.status.p, 0, sizeof(int32_t) * replicas, ctx->stream));
-  LABS_CUDA(cudaMemsetAsync(b.counter.p, 0, sizeof(int32_t), ctx->stream));
-  LABS_CUDA(cudaMemsetAsync(b.stop.p, 0, sizeof(int32_t), ctx->stream));
-  LABS_CUDA(cudaMemsetAsync(b.order.p, 0xff, sizeof(int32_t) * replicas, ctx->stream));
-  if (mt) {
-    k_seed<<<(replicas + 127) / 128, 128, 0, ctx->stream>>>(replicas, base_seed,
-                                                             b.mt.as<labs_rng_state>());
+  cudaStream_t st = ctx->stream;
+  LABS_CUDA(cudaMemsetAsync(s->init.p, 0, sizeof(int32_t) * R, st));
+  LABS_CUDA(cudaMemsetAsync(s->status.p, 0, sizeof(int32_t) * R, st));
+  LABS_CUDA(cudaMemsetAsync(s->iters.p, 0, sizeof(int64_t) * R, st));
+  LABS_CUDA(cudaMemsetAsync(s->counter.p, 0, sizeof(int32_t), st));
+  LABS_CUDA(cudaMemsetAsync(s->stop.p, 0, sizeof(int32_t), st));
+  LABS_CUDA(cudaMemsetAsync(s->tabu_total.p, 0, sizeof(unsigned long long), st));
+  LABS_CUDA(cudaMemsetAsync(s->tabu_rep.p, 0, sizeof(int64_t) * R, st));
+  LABS_CUDA(cudaMemsetAsync(s->order.p, 0xff, sizeof(int32_t) * R, st));
+  if (trace_cap) LABS_CUDA(cudaMemsetAsync(s->trace_len.p, 0, sizeof(int64_t) * R, st));
+  if (s->mt) {
+    k_seed<<<(replicas + 127) / 128, 128, 0, st>>>(
+        replicas, base_seed + static_cast<uint64_t>(replica_offset), s->rng.as<labs_rng_state>());
     LABS_CUDA(cudaGetLastError());
   } else {
-    LABS_CUDA(cudaMemsetAsync(b.ctr.p, 0, sizeof(uint64_t) * replicas, ctx->stream));
+    LABS_CUDA(cudaMemsetAsync(s->ctr.p, 0, sizeof(uint64_t) * R, st));
   }
-  MemeticArgs A{};
+  MemeticArgs& A = s->A;
   A.n = n;
-  A.nw = nw;
+  A.nw = s->nw;
   A.replicas = replicas;
-  A.K = K;
-  A.p_comb = p->p_comb;
-  A.p_mutate = p->p_mutate > 0.0 ? p->p_mutate : 1.0 / n;
-  A.target = p->target_energy;
-  A.max_ns = p->max_seconds >= 0 ? static_cast<int64_t>(p->max_seconds * 1e9) : -1;
-  A.max_iterations = p->max_iterations;
-  A.tabu = to_cfg(&p->tabu);
-  A.race = race;
+  A.K = s->K;
+  A.p_comb = params->p_comb;
+  A.p_mutate = params->p_mutate > 0.0 ? params->p_mutate : 1.0 / n;
+  A.target = params->target_energy;
+  A.max_ns = params->max_seconds >= 0 ? static_cast<int64_t>(params->max_seconds * 1e9) : -1;
+  A.max_iterations = params->max_iterations;
+  A.epoch_iters = -1;
+  A.epoch_ns = -1;
+  A.crossover = params->crossover;
+  A.replacement = params->replacement;
+  A.tabu = to_cfg(&params->tabu);
+  A.race = 1;
   A.base_seed = base_seed;
-  A.pop = b.pop.as<uint64_t>();
-  A.popE = b.popE.as<int32_t>();
-  A.best = b.best.as<uint64_t>();
-  A.bestE = b.bestE.as<int32_t>();
-  A.iters = b.iters.as<int64_t>();
-  A.status = b.status.as<int32_t>();
-  A.initialized = b.init.as<int32_t>();
-  A.t0 = b.t0.as<int64_t>();
-  A.t_end = b.tend.as<int64_t>();
-  A.pub_order = b.order.as<int32_t>();
-  A.pub_counter = b.counter.as<int32_t>();
-  A.mt = mt ? b.mt.as<labs_rng_state>() : nullptr;
-  A.ctr = mt ? nullptr : b.ctr.as<uint64_t>();
-  A.stop = b.stop.as<int32_t>();
-  A.tabu_iters = nullptr;
-  A.trace = traces ? b.trace.as<int64_t>() : nullptr;
-  A.trace_cap = traces ? trace_cap : 0;
-  A.trace_len = traces ? b.trace_len.as<int64_t>() : nullptr;
-  // With a host stop flag, run in epochs and forward the flag in between.
-  A.epoch_iters = host_stop ? 8 : -1;
-  std::vector<int32_t> status(replicas);
-  for (;;) {
-    if (host_stop && *host_stop) {
-      const int32_t one = 1;
-      LABS_H2D(b.stop.p, &one, sizeof(int32_t));
-    }
-    int rc = dispatch(n, [&](auto ns) -> int {
-      constexpr int NS = decltype(ns)::value;
-      if (mt) {
-        const size_t smem = kWarps * slot_bytes<NS, true>();
-        auto kern = k_memetic<NS, true>;
-        if (int r = prep(kern, smem)) return r;
-        int grid = 0;
-        if (int r = grid_for(ctx, kern, smem, replicas, &grid)) return r;
-        kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
-      } else {
-        const size_t smem = kWarps * slot_bytes<NS, false>();
-        auto kern = k_memetic<NS, false>;
-        if (int r = prep(kern, smem)) return r;
-        int grid = 0;
-        if (int r = grid_for(ctx, kern, smem, replicas, &grid)) return r;
-        kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
-      }
-      LABS_CUDA(cudaGetLastError());
-      return LABS_OK;
-    });
-    if (rc) return rc;
-    LABS_D2H(status.data(), b.status.p, sizeof(int32_t) * replicas);
-    LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-    bool done = true;
-    for (int r = 0; r < replicas; ++r) done &= status[r] != kRunning;
-    if (done) break;
+  A.replica_offset = replica_offset;
+  A.pop = s->pop.as<uint64_t>();
+  A.popE = s->popE.as<int32_t>();
+  A.best = s->best.as<uint64_t>();
+  A.bestE = s->bestE.as<int32_t>();
+  A.iters = s->iters.as<int64_t>();
+  A.status = s->status.as<int32_t>();
+  A.initialized = s->init.as<int32_t>();
+  A.t0 = s->t0.as<int64_t>();
+  A.t_end = s->tend.as<int64_t>();
+  A.pub_order = s->order.as<int32_t>();
+  A.pub_counter = s->counter.as<int32_t>();
+  A.mt = s->mt ? s->rng.as<labs_rng_state>() : nullptr;
+  A.ctr = s->mt ? nullptr : s->ctr.as<uint64_t>();
+  A.stop = s->stop.as<int32_t>();
+  A.tabu_iters = s->tabu_total.as<unsigned long long>();
+  A.tabu_per_replica = s->tabu_rep.as<int64_t>();
+  A.trace = trace_cap ? s->trace.as<int64_t>() : nullptr;
+  A.trace_cap = trace_cap;
+  A.trace_len = trace_cap ? s->trace_len.as<int64_t>() : nullptr;
+  *out = guard.release();
+  return LABS_OK;
+}
+
+int labs_solver_destroy(labs_solver* s) {
+  if (!s) return LABS_OK;
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  delete s;
+  return LABS_OK;
+}
+
+int labs_solver_run(labs_solver* s, int64_t epoch_iterations, double epoch_seconds, int race) {
+  if (!s) return fail(LABS_ERR_INVALID_ARGUMENT, "null solver");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  MemeticArgs A = s->A;
+  A.epoch_iters = epoch_iterations;
+  A.epoch_ns = epoch_seconds >= 0 ? static_cast<int64_t>(epoch_seconds * 1e9) : -1;
+  A.race = race ? 1 : 0;
+  return dispatch(s->n, [&](auto ns) -> int {
+    constexpr int NS = decltype(ns)::value;
+    return s->mt ? launch_memetic<NS, true>(ctx, A) : launch_memetic<NS, false>(ctx, A);
+  });
+}
+
+int labs_solver_request_stop(labs_solver* s) {
+  if (!s) return fail(LABS_ERR_INVALID_ARGUMENT, "null solver");
+  labs_ctx* ctx = s->ctx;
+  static const int32_t one = 1;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  LABS_H2D(s->stop.p, &one, sizeof(int32_t));
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LABS_OK;
+}
+
+int labs_solver_status(labs_solver* s, int32_t* running, int64_t* best_energy,
+                       int32_t* best_replica) {
+  if (!s) return fail(LABS_ERR_INVALID_ARGUMENT, "null solver");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  std::vector<int32_t> st(s->R), be(s->R), init(s->R);
+  LABS_D2H(st.data(), s->status.p, sizeof(int32_t) * s->R);
+  LABS_D2H(be.data(), s->bestE.p, sizeof(int32_t) * s->R);
+  LABS_D2H(init.data(), s->init.p, sizeof(int32_t) * s->R);
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  LABS_CUDA(cudaGetLastError());
+  int run = 0, arg = -1;
+  for (int r = 0; r < s->R; ++r) {
+    run += (!init[r] || st[r] == kRunning) ? 1 : 0;
+    if (init[r] && (arg < 0 || be[r] < be[arg])) arg = r;
   }
-  std::vector<uint64_t> best(static_cast<size_t>(replicas) * nw);
-  std::vector<int32_t> bestE(replicas), order(replicas);
-  std::vector<int64_t> iters(replicas), t0(replicas), tend(replicas);
-  LABS_D2H(best.data(), b.best.p, sizeof(uint64_t) * replicas * nw);
-  LABS_D2H(bestE.data(), b.bestE.p, sizeof(int32_t) * replicas);
-  LABS_D2H(iters.data(), b.iters.p, sizeof(int64_t) * replicas);
-  LABS_D2H(t0.data(), b.t0.p, sizeof(int64_t) * replicas);
-  LABS_D2H(tend.data(), b.tend.p, sizeof(int64_t) * replicas);
-  LABS_D2H(order.data(), b.order.p, sizeof(int32_t) * replicas);
+  if (running) *running = run;
+  if (best_energy) *best_energy = arg >= 0 ? be[arg] : -1;
+  if (best_replica) *best_replica = arg >= 0 ? static_cast<int32_t>(arg + s->offset) : -1;
+  return LABS_OK;
+}
+
+int labs_solver_counters(labs_solver* s, uint64_t* tabu_iterations, int64_t* memetic_iterations) {
+  if (!s) return fail(LABS_ERR_INVALID_ARGUMENT, "null solver");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  unsigned long long t = 0;
+  std::vector<int64_t> it(s->R);
+  LABS_D2H(&t, s->tabu_total.p, sizeof(t));
+  LABS_D2H(it.data(), s->iters.p, sizeof(int64_t) * s->R);
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (tabu_iterations) *tabu_iterations = t;
+  if (memetic_iterations) {
+    int64_t sum = 0;
+    for (int64_t v : it) sum += v;
+    *memetic_iterations = sum;
+  }
+  return LABS_OK;
+}
+
+int labs_solver_results(labs_solver* s, labs_run_result* per_replica, labs_memetic_record* traces,
+                        int64_t* trace_len, int32_t* publish_order) {
+  if (!s || !per_replica) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  const int R = s->R, nw = s->nw;
+  std::vector<uint64_t> best(static_cast<size_t>(R) * nw);
+  std::vector<int32_t> bestE(R), order(R), status(R);
+  std::vector<int64_t> iters(R), t0(R), tend(R), tabu(R);
+  LABS_D2H(best.data(), s->best.p, sizeof(uint64_t) * R * nw);
+  LABS_D2H(bestE.data(), s->bestE.p, sizeof(int32_t) * R);
+  LABS_D2H(iters.data(), s->iters.p, sizeof(int64_t) * R);
+  LABS_D2H(t0.data(), s->t0.p, sizeof(int64_t) * R);
+  LABS_D2H(tend.data(), s->tend.p, sizeof(int64_t) * R);
+  LABS_D2H(order.data(), s->order.p, sizeof(int32_t) * R);
+  LABS_D2H(status.data(), s->status.p, sizeof(int32_t) * R);
+  LABS_D2H(tabu.data(), s->tabu_rep.p, sizeof(int64_t) * R);
   std::vector<int64_t> tr, tl;
-  if (traces) {
-    tr.resize(static_cast<size_t>(3) * replicas * std::max<int64_t>(trace_cap, 1));
-    tl.resize(replicas);
-    LABS_D2H(tr.data(), b.trace.p, sizeof(int64_t) * tr.size());
-    LABS_D2H(tl.data(), b.trace_len.p, sizeof(int64_t) * replicas);
+  if (traces && s->trace_cap) {
+    tr.resize(static_cast<size_t>(3) * R * s->trace_cap);
+    tl.resize(R);
+    LABS_D2H(tr.data(), s->trace.p, sizeof(int64_t) * tr.size());
+    LABS_D2H(tl.data(), s->trace_len.p, sizeof(int64_t) * R);
   }
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int r = 0; r < replicas; ++r) {
+  LABS_CUDA(cudaGetLastError());
+  for (int r = 0; r < R; ++r) {
     labs_run_result& o = per_replica[r];
     std::memset(&o, 0, sizeof(o));
     for (int wi = 0; wi < nw; ++wi) o.best[wi] = best[static_cast<size_t>(r) * nw + wi];
     o.best_energy = bestE[r];
-    o.merit = static_cast<double>(n) * n / (2.0 * static_cast<double>(bestE[r]));
+    o.merit = static_cast<double>(s->n) * s->n / (2.0 * static_cast<double>(bestE[r]));
     o.iterations = iters[r];
-    o.wall_seconds = 1e-9 * static_cast<double>(tend[r] - t0[r]);
-    o.seed = base_seed + static_cast<uint64_t>(r);
-    o.replica_id = r;
-    o.reached_target = bestE[r] <= p->target_energy;
-    if (traces) {
-      const int64_t len = std::min(tl[r], trace_cap);
-      trace_len[r] = len;
+    o.wall_seconds = status[r] != kRunning ? 1e-9 * static_cast<double>(tend[r] - t0[r]) : 0.0;
+    o.seed = s->base_seed + static_cast<uint64_t>(s->offset + r);
+    o.replica_id = static_cast<int32_t>(s->offset + r);
+    o.reached_target = bestE[r] <= s->p.target_energy;
+    o.tabu_iterations = tabu[r];
+    if (traces && s->trace_cap) {
+      const int64_t len = std::min(tl[r], s->trace_cap);
+      if (trace_len) trace_len[r] = len;
       for (int64_t i = 0; i < len; ++i) {
-        const int64_t* rec = &tr[(static_cast<size_t>(r) * trace_cap + i) * 3];
-        labs_memetic_record& d = traces[static_cast<size_t>(r) * trace_cap + i];
+        const int64_t* rec = &tr[(static_cast<size_t>(r) * s->trace_cap + i) * 3];
+        labs_memetic_record& d = traces[static_cast<size_t>(r) * s->trace_cap + i];
         d.iteration = rec[0];
         d.stop_seen = static_cast<int32_t>(rec[1]);
         d.pad_ = 0;
@@ -898,13 +1119,36 @@ int run_memetic(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
       }
     }
   }
-  if (order_out) *order_out = order;
+  if (publish_order) std::memcpy(publish_order, order.data(), sizeof(int32_t) * R);
   return LABS_OK;
 }
 
-}  // namespace
+int labs_solver_export_elites(labs_solver* s, int k, uint64_t* d_words, int64_t* d_energies) {
+  if (!s || k < 1 || !d_words || !d_energies)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (k > s->R) return fail(LABS_ERR_INVALID_ARGUMENT, "k exceeds the replica count");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  k_export_elites<<<1, 1024, 0, ctx->stream>>>(s->R, s->nw, k, s->bestE.as<int32_t>(),
+                                                s->best.as<uint64_t>(), s->taken.as<int32_t>(),
+                                                d_words, d_energies);
+  LABS_CUDA(cudaGetLastError());
+  return LABS_OK;
+}
 
-extern "C" {
+int labs_solver_import_elites(labs_solver* s, int count, const uint64_t* d_words,
+                              const int64_t* d_energies, int rotation) {
+  if (!s || count < 1 || !d_words || !d_energies || rotation < 0)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  const int wpb = 8;
+  k_import_elites<<<(s->R + wpb - 1) / wpb, 32 * wpb, 0, ctx->stream>>>(
+      s->R, s->nw, s->K, count, rotation, d_words, d_energies, s->pop.as<uint64_t>(),
+      s->popE.as<int32_t>(), s->status.as<int32_t>());
+  LABS_CUDA(cudaGetLastError());
+  return LABS_OK;
+}
 
 int labs_memetic(labs_ctx* ctx, int n, const labs_memetic_params* params, uint64_t seed,
                  const volatile int32_t* stop, int replica_id, labs_run_result* out,
@@ -913,13 +1157,22 @@ int labs_memetic(labs_ctx* ctx, int n, const labs_memetic_params* params, uint64
   if (!ctx || !out) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
   if (trace && (trace_cap < 0 || !trace_len))
     return fail(LABS_ERR_INVALID_ARGUMENT, "trace needs a capacity and a length output");
-  int64_t tl = 0;
-  int rc = run_memetic(ctx, n, 1, seed, params, stop, 0, out, trace, trace_cap,
-                       trace ? &tl : nullptr, nullptr);
-  if (rc) return rc;
+  labs_solver* s = nullptr;
+  if (int rc = labs_solver_create(ctx, n, 1, seed, 0, params, trace ? trace_cap : 0, &s))
+    return rc;
+  std::unique_ptr<labs_solver, int (*)(labs_solver*)> guard(s, labs_solver_destroy);
+  // With a host stop flag, run in epochs and forward the flag in between.
+  for (;;) {
+    if (stop && *stop)
+      if (int rc = labs_solver_request_stop(s)) return rc;
+    if (int rc = labs_solver_run(s, stop ? 8 : -1, -1.0, 0)) return rc;
+    int32_t running = 0;
+    if (int rc = labs_solver_status(s, &running, nullptr, nullptr)) return rc;
+    if (!running) break;
+  }
+  if (int rc = labs_solver_results(s, out, trace, trace_len, nullptr)) return rc;
   out->seed = seed;
   out->replica_id = replica_id;
-  if (trace_len) *trace_len = tl;
   return LABS_OK;
 }
 
@@ -933,11 +1186,15 @@ int labs_run_replicas(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   if (!ctx || !out) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
   if (traces && (trace_cap < 0 || !trace_len))
     return fail(LABS_ERR_INVALID_ARGUMENT, "traces need a capacity and length outputs");
+  labs_solver* s = nullptr;
+  if (int rc = labs_solver_create(ctx, n, replicas, base_seed, 0, params, traces ? trace_cap : 0,
+                                  &s))
+    return rc;
+  std::unique_ptr<labs_solver, int (*)(labs_solver*)> guard(s, labs_solver_destroy);
+  if (int rc = labs_solver_run(s, -1, -1.0, 1)) return rc;
   std::vector<labs_run_result> per(replicas);
-  std::vector<int32_t> order;
-  int rc = run_memetic(ctx, n, replicas, base_seed, params, nullptr, 1, per.data(), traces,
-                       trace_cap, trace_len, &order);
-  if (rc) return rc;
+  std::vector<int32_t> order(replicas);
+  if (int rc = labs_solver_results(s, per.data(), traces, trace_len, order.data())) return rc;
   // SharedState::publish (parallel.cpp:10-15): strictly lower energy wins;
   // among equal energies the earliest publisher keeps the slot.
   int win = 0;
@@ -952,3 +1209,31 @@ int labs_run_replicas(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
 }
 
 }  // extern "C"
+
+extern "C" int labs_bench_int_peak(labs_ctx* ctx, double* gops) {
+  if (!ctx || !gops) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  DBuf sink;
+  LABS_ALLOC(sink, sizeof(int));
+  const int blocks = ctx->sm_count * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  LABS_CUDA(cudaEventCreate(&e0));
+  LABS_CUDA(cudaEventCreate(&e1));
+  k_int_peak<<<blocks, threads, 0, ctx->stream>>>(64, 3, sink.as<int>());  // warm-up
+  float best_ms = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    LABS_CUDA(cudaEventRecord(e0, ctx->stream));
+    k_int_peak<<<blocks, threads, 0, ctx->stream>>>(iters, 3 + rep, sink.as<int>());
+    LABS_CUDA(cudaEventRecord(e1, ctx->stream));
+    LABS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    LABS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    best_ms = std::min(best_ms, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  LABS_CUDA(cudaGetLastError());
+  const double ops = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+  *gops = ops / (best_ms * 1e-3) / 1e9;
+  return LABS_OK;
+}

@@ -31,9 +31,13 @@ struct MemeticArgs {
   int64_t max_ns;          // < 0: unlimited (max_seconds)
   int64_t max_iterations;  // < 0: unlimited
   int64_t epoch_iters;     // < 0: run to completion in this launch
+  int64_t epoch_ns;        // < 0: no per-launch time slice
+  int crossover;           // 0 uniform (reference), 1 one-point
+  int replacement;         // 0 random victim (reference), 1 worst if better
   TabuCfg tabu;
   int race;                // raise *stop when a replica reaches the target
   uint64_t base_seed;      // Philox key
+  int64_t replica_offset;  // global id of local replica 0
   // replica state (global memory)
   uint64_t* pop;           // R x K x nw
   int32_t* popE;           // R x K
@@ -50,6 +54,7 @@ struct MemeticArgs {
   uint64_t* ctr;           // R (Philox mode)
   volatile int32_t* stop;  // device-resident stop flag
   unsigned long long* tabu_iters;  // accumulated tabu iterations (optional)
+  int64_t* tabu_per_replica;       // R, tabu iterations per replica
   // optional trace
   int64_t* trace;          // R x cap x 3 {iteration, stop_seen, child_energy}
   int64_t trace_cap;
@@ -126,6 +131,21 @@ __device__ __forceinline__ void mutate_chunks(uint32_t (&c)[NS], int n,
   }
 }
 
+// First index of the maximum energy (warp-parallel scan over K entries).
+__device__ __forceinline__ int worst_member(const int32_t* e, int K) {
+  long long best = -1;
+  for (int i = lane_id(); i < K; i += 32) {
+    const long long key = (static_cast<long long>(e[i]) << 32) | (0x7fffffff - i);
+    best = key > best ? key : best;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const long long other = __shfl_xor_sync(kFull, best, o);
+    best = other > best ? other : best;
+  }
+  return 0x7fffffff - static_cast<int>(best & 0xffffffffLL);
+}
+
 template <class R>
 __device__ __forceinline__ int tournament(const int32_t* e, int K, R& rng) {
   const int a = static_cast<int>(uniform_int(rng, 0, K - 1));
@@ -188,6 +208,7 @@ __device__ void memetic_replica(const MemeticArgs& A, int r, Walker<NS>& w,
   const int64_t t0 = A.t0[r];
   int64_t tlen = A.trace_len ? A.trace_len[r] : 0;
   const int64_t it_start = it;
+  const int64_t resume_ns = globaltimer_ns();
   int32_t st = kRunning;
   unsigned long long tabu_steps = 0;
   while (true) {
@@ -216,6 +237,7 @@ __device__ void memetic_replica(const MemeticArgs& A, int r, Walker<NS>& w,
       break;
     }
     if (A.epoch_iters >= 0 && it - it_start >= A.epoch_iters) break;  // epoch
+    if (A.epoch_ns >= 0 && globaltimer_ns() - resume_ns >= A.epoch_ns) break;
 
     uint32_t child[NS];
     if (uniform01(rng) < A.p_comb) {
@@ -224,14 +246,25 @@ __device__ void memetic_replica(const MemeticArgs& A, int r, Walker<NS>& w,
       uint32_t a[NS], b[NS];
       load_seq<NS>(pop + static_cast<size_t>(p1) * nw, nw, a);
       load_seq<NS>(pop + static_cast<size_t>(p2) * nw, nw, b);
+      if (A.crossover == 0) {
+        // combine (memetic.cpp:24-33): one bits64() mask per 64-bit word.
 #pragma unroll
-      for (int wi = 0; wi < (NS + 1) / 2; ++wi) {
-        const uint64_t mask = rng.next();  // one bits64() per word
-        const uint32_t mlo = static_cast<uint32_t>(mask);
-        const uint32_t mhi = static_cast<uint32_t>(mask >> 32);
-        child[2 * wi] = (a[2 * wi] & mlo) | (b[2 * wi] & ~mlo);
-        if (2 * wi + 1 < NS)
-          child[2 * wi + 1] = (a[2 * wi + 1] & mhi) | (b[2 * wi + 1] & ~mhi);
+        for (int wi = 0; wi < (NS + 1) / 2; ++wi) {
+          const uint64_t mask = rng.next();
+          const uint32_t mlo = static_cast<uint32_t>(mask);
+          const uint32_t mhi = static_cast<uint32_t>(mask >> 32);
+          child[2 * wi] = (a[2 * wi] & mlo) | (b[2 * wi] & ~mlo);
+          if (2 * wi + 1 < NS)
+            child[2 * wi + 1] = (a[2 * wi + 1] & mhi) | (b[2 * wi + 1] & ~mhi);
+        }
+      } else {
+        // one-point: positions [0, cut) from parent 1, [cut, n) from parent 2.
+        const int cut = static_cast<int>(uniform_int(rng, 1, n - 1));
+#pragma unroll
+        for (int b2 = 0; b2 < NS; ++b2) {
+          const uint32_t m1 = lowmask(cut - 32 * b2);
+          child[b2] = (a[b2] & m1) | (b[b2] & ~m1);
+        }
       }
 #pragma unroll
       for (int b2 = 0; b2 < NS; ++b2) child[b2] &= lowmask(n - 32 * b2);
@@ -249,9 +282,19 @@ __device__ void memetic_replica(const MemeticArgs& A, int r, Walker<NS>& w,
       bestE = re;
       store_chunks<NS>(best, nw, refined);
     }
-    const int victim = static_cast<int>(uniform_int(rng, 0, K - 1));
-    store_chunks<NS>(pop + static_cast<size_t>(victim) * nw, nw, refined);
-    if (ln == 0) popE[victim] = re;
+    if (A.replacement == 0) {
+      // memetic.cpp:100-102: uniform victim, best not protected.
+      const int victim = static_cast<int>(uniform_int(rng, 0, K - 1));
+      store_chunks<NS>(pop + static_cast<size_t>(victim) * nw, nw, refined);
+      if (ln == 0) popE[victim] = re;
+    } else {
+      // elite-preserving: the child displaces the worst member if better.
+      const int victim = worst_member(popE, K);
+      if (re < popE[victim]) {
+        store_chunks<NS>(pop + static_cast<size_t>(victim) * nw, nw, refined);
+        if (ln == 0) popE[victim] = re;
+      }
+    }
     if (A.trace && tlen < A.trace_cap && ln == 0) {
       int64_t* rec = A.trace + (static_cast<size_t>(r) * A.trace_cap + tlen) * 3;
       rec[0] = it;
@@ -269,6 +312,7 @@ __device__ void memetic_replica(const MemeticArgs& A, int r, Walker<NS>& w,
     A.iters[r] = it;
     if (A.trace_len) A.trace_len[r] = tlen;
     if (A.tabu_iters) atomicAdd(A.tabu_iters, tabu_steps);
+    if (A.tabu_per_replica) A.tabu_per_replica[r] += static_cast<int64_t>(tabu_steps);
     if (st != kRunning) {
       A.status[r] = st;
       A.t_end[r] = globaltimer_ns();

@@ -1,0 +1,248 @@
+// Tests of the labsolve:: drop-in, written against the reference's public
+// headers (proj/include/labsolve/*.hpp) the way its own doctest suites use
+// them (proj/tests/test_{sequence,correlation,tabu,memetic,parallel}.cpp),
+// so the same calls and expectations hold on the B200 implementation.
+#include <cstdio>
+#include <functional>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "labsolve/correlation_state.hpp"
+#include "labsolve/memetic.hpp"
+#include "labsolve/parallel.hpp"
+#include "labsolve/sequence.hpp"
+#include "labsolve/tabu.hpp"
+
+using namespace labsolve;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    ++g_checks;                                                              \
+    if (!(cond)) {                                                           \
+      ++g_fail;                                                              \
+      std::fprintf(stderr, "%s:%d: CHECK(%s) failed\n", __FILE__, __LINE__, #cond); \
+    }                                                                        \
+  } while (0)
+#define CHECK_THROWS_AS(expr, type)                                          \
+  do {                                                                       \
+    ++g_checks;                                                              \
+    bool ok_ = false;                                                        \
+    try {                                                                    \
+      (void)(expr);                                                          \
+    } catch (const type&) {                                                  \
+      ok_ = true;                                                            \
+    } catch (...) {                                                          \
+    }                                                                        \
+    if (!ok_) {                                                              \
+      ++g_fail;                                                              \
+      std::fprintf(stderr, "%s:%d: %s did not throw %s\n", __FILE__, __LINE__, #expr, #type); \
+    }                                                                        \
+  } while (0)
+
+static long long naive_energy(const Sequence& s) {
+  long long e = 0;
+  for (int k = 1; k < s.size(); ++k) {
+    long long c = 0;
+    for (int i = 0; i + k < s.size(); ++i) c += s.spin(i) * s.spin(i + k);
+    e += c * c;
+  }
+  return e;
+}
+
+static void sequences() {
+  Sequence s = decode_hex("EE01C0E77667DD34DAE94B5", 92);
+  CHECK(energy(s) == 490);
+  CHECK(encode_hex(s) == "EE01C0E77667DD34DAE94B5");
+  CHECK(decode_hex("8", 4).spin(0) == -1);
+  CHECK_THROWS_AS(decode_hex("F", 3), std::invalid_argument);
+  CHECK_THROWS_AS(energy(Sequence(1)), std::invalid_argument);
+  Rng rng(17);
+  std::vector<Sequence> batch;
+  for (int i = 0; i < 50; ++i) batch.push_back(Sequence::random(77, rng));
+  std::vector<long long> e = energies(batch);
+  for (int i = 0; i < 50; ++i) CHECK(e[i] == naive_energy(batch[i]));
+  Sequence c = canonical(batch[0]);
+  CHECK(energy(c) == e[0]);
+  CHECK(energy(reversed(batch[1])) == e[1]);
+  CHECK(energy(complement(batch[2])) == e[2]);
+}
+
+static void correlation() {
+  CorrelationState st(Sequence::all_plus(5));
+  CHECK(st.energy() == 30);
+  CHECK(st.correlation(1) == 4 && st.correlation(4) == 1);
+  CHECK_THROWS_AS(st.correlation(0), std::out_of_range);
+  CorrelationState sq(Sequence::all_plus(4));
+  for (int j = 0; j < 4; ++j) CHECK(sq.neighbor_energy(j) == 2);
+  CHECK_THROWS_AS(sq.neighbor_energy(4), std::out_of_range);
+  std::map<int, std::size_t> bytes{{2, 1}, {11, 7}, {92, 524}, {187, 2174}};
+  for (auto [n, b] : bytes) CHECK(CorrelationState(Sequence::all_plus(n)).table_bytes() == b);
+  Rng rng(43);
+  for (int n : {8, 33, 64, 128}) {
+    Sequence s = Sequence::random(n, rng);
+    CorrelationState cs(s);
+    for (int step = 0; step < 40; ++step) {
+      int j = static_cast<int>(rng.uniform_int(0, n - 1));
+      long long promised = cs.neighbor_energy(j);
+      std::uint64_t touched = 0;
+      cs.apply_flip(j, &touched);
+      CHECK(touched == static_cast<std::uint64_t>(n - 1));
+      CHECK(cs.energy() == promised);
+    }
+    CHECK(cs.energy() == naive_energy(cs.pivot()));
+  }
+  // ties resolve uniformly (test_correlation.cpp:176-191), smaller sample
+  std::map<int, int> hits;
+  Rng r2(59);
+  const int trials = 4000;
+  for (int t = 0; t < trials; ++t) {
+    ScanResult p = scan_neighborhood(sq, [](int) { return true; }, r2);
+    CHECK(p.energy == 2);
+    ++hits[p.position];
+  }
+  for (int j = 0; j < 4; ++j) CHECK(hits[j] > trials / 4 - trials / 16 && hits[j] < trials / 4 + trials / 16);
+  CorrelationState six(Sequence::all_plus(6));
+  CHECK_THROWS_AS(scan_neighborhood(six, [](int) { return false; }, r2, 1, false),
+                  std::runtime_error);
+  ScanResult fb = scan_neighborhood(six, [](int) { return false; }, r2);
+  CHECK(fb.fallback && fb.energy == six.neighbor_energy(fb.position));
+}
+
+static void tabu() {
+  Rng rng(73);
+  for (int trial = 0; trial < 20; ++trial) {
+    TabuTrace trace;
+    tabu_search(Sequence::random(25, rng), TabuParams{}, rng, 1, &trace);
+    CHECK(trace.max_iter >= 12 && trace.max_iter <= 37);
+    CHECK(trace.min_tabu == trace.max_iter / 10);
+    CHECK(trace.max_tabu == 3 * trace.max_iter / 25);
+    CHECK(static_cast<int>(trace.steps.size()) == trace.max_iter);
+  }
+  Sequence s8 = Sequence::all_plus(8);
+  CHECK_THROWS_AS(tabu_search(Sequence::all_plus(1), TabuParams{}, rng), std::invalid_argument);
+  CHECK_THROWS_AS(tabu_search(s8, TabuParams{0.2, 0.1}, rng), std::invalid_argument);
+  CHECK_THROWS_AS(tabu_search(s8, TabuParams{0.5, 1.0}, rng), std::invalid_argument);
+  CHECK_THROWS_AS(tabu_search(s8, TabuParams{}, rng, 0), std::invalid_argument);
+  Rng r97(97);
+  for (int trial = 0; trial < 20; ++trial) {
+    int n = 4 + static_cast<int>(r97.uniform_int(0, 28));
+    TabuTrace trace;
+    Sequence start = Sequence::random(n, r97);
+    TabuResult res = tabu_search(start, TabuParams{}, r97, 1, &trace);
+    std::vector<long long> expiry(n, 0);
+    long long floor_seen = naive_energy(start);
+    for (const TabuStep& st : trace.steps) {
+      if (!st.fallback) CHECK(expiry[st.position] < st.iteration);
+      expiry[st.position] = st.iteration + st.tenure;
+      floor_seen = std::min(floor_seen, st.energy);
+    }
+    CHECK(res.energy == floor_seen && res.energy == naive_energy(res.best));
+  }
+  Rng seed_rng(103);
+  Sequence start = Sequence::random(32, seed_rng);
+  auto run = [&](int workers) {
+    Rng r(104729);
+    TabuTrace trace;
+    TabuResult res = tabu_search(start, TabuParams{}, r, workers, &trace);
+    return std::make_tuple(res.best, res.energy, trace.steps.back().position, r.bits64());
+  };
+  CHECK(run(1) == run(1));
+  CHECK(run(2) == run(1));
+  TabuTrace t;
+  t.max_iter = 3;
+  t.steps.push_back({1, 4, 22, 0, false});
+  t.steps.push_back({2, 0, 18, 0, true});
+  CHECK(format_trace(t) == "maxIter 3 tenure [0,0]\n1 4 22 0\n2 0 18 0 fallback\n");
+}
+
+static void memetic() {
+  MemeticParams p;
+  p.target_energy = 26;
+  RunResult r = memetic_tabu(20, p, 43);
+  CHECK(r.reached_target && r.best_energy == 26 && r.iterations == 98);
+  CHECK(encode_hex(r.best) == "C9EF5");
+  Rng rng(5);
+  std::vector<long long> e{5, 1, 9, 1};
+  int first_wins = 0;
+  for (int t = 0; t < 2000; ++t) {
+    auto [a, b] = select_parents({1, 2}, rng);
+    first_wins += (a == 0) + (b == 0);
+  }
+  CHECK(first_wins > 2800 && first_wins < 3200);  // P = 3/4 per pick
+  Sequence c = combine(Sequence::all_plus(64), complement(Sequence::all_plus(64)), rng);
+  CHECK(c.size() == 64);
+  CHECK_THROWS_AS(mutate(c, 0.0, rng), std::invalid_argument);
+  MemeticParams bad;
+  bad.population_size = 1;
+  CHECK_THROWS_AS(memetic_tabu(12, bad, 1), std::invalid_argument);
+  MemeticParams few;
+  few.target_energy = 0;
+  few.max_iterations = 5;
+  MemeticTrace trace;
+  RunResult a = memetic_tabu(30, few, 11, nullptr, &trace);
+  RunResult b = memetic_tabu(30, few, 11);
+  CHECK(a.best == b.best && a.iterations == 5 && trace.iters.size() == 5);
+  std::atomic<bool> stop{true};
+  MemeticTrace st;
+  RunResult s = memetic_tabu(30, few, 11, &stop, &st);
+  CHECK(s.iterations == 0 && st.iters.size() == 1 && st.iters[0].stop_seen);
+}
+
+static void parallel() {
+  MemeticParams params;
+  params.target_energy = 0;
+  params.max_iterations = 20;
+  RunResult bare = memetic_tabu(18, params, 777);
+  ParallelConfig cfg;
+  cfg.n = 18;
+  cfg.replicas = 1;
+  cfg.base_seed = 777;
+  cfg.memetic = params;
+  RunResult wrapped = run_replicas(cfg);
+  CHECK(wrapped.best == bare.best && wrapped.iterations == bare.iterations);
+  CHECK(wrapped.seed == bare.seed && wrapped.replica_id == 0);
+  SharedState state;
+  RunResult x;
+  x.best_energy = 50;
+  x.replica_id = 1;
+  CHECK(state.publish(x));
+  x.replica_id = 2;
+  CHECK(!state.publish(x));
+  CHECK(state.best()->replica_id == 1);
+  CHECK(suggested_scan_workers(107) == 128);
+  CHECK(suggested_replicas(148, 32, 2048, 128) == 2368);
+  CHECK(shared_footprint(187, 100) == 5258);
+  ParallelConfig race;
+  race.n = 16;
+  race.replicas = 6;
+  race.base_seed = 20000;
+  race.memetic.target_energy = 24;  // proven optimum for n = 16
+  race.memetic.max_seconds = 60.0;
+  ReplicaReport report;
+  report.collect_traces = true;
+  RunResult res = run_replicas(race, &report);
+  CHECK(res.reached_target && res.best_energy == 24 && naive_energy(res.best) == 24);
+  CHECK(res.seed == race.base_seed + static_cast<std::uint64_t>(res.replica_id));
+  CHECK(report.results.size() == 6 && report.traces.size() == 6);
+  ParallelConfig broken;
+  broken.n = 12;
+  broken.replicas = 3;
+  broken.memetic.population_size = 1;
+  CHECK_THROWS_AS(run_replicas(broken), std::invalid_argument);
+  broken.replicas = 0;
+  CHECK_THROWS_AS(run_replicas(broken), std::invalid_argument);
+}
+
+int main() {
+  sequences();
+  correlation();
+  tabu();
+  memetic();
+  parallel();
+  std::printf("%d checks, %d failed\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}

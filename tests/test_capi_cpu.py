@@ -65,6 +65,6 @@ def test_struct_layouts_match_header():
     assert C.sizeof(capi.RngState) == 312 * 8 + 8
     assert C.sizeof(capi.TabuStep) == 24
     assert C.sizeof(capi.TabuParams) == 24
-    assert C.sizeof(capi.MemeticParams) == 4 + 4 + 8 * 5 + 24
-    assert C.sizeof(capi.RunResult) == 8 * 4 + 8 * 5 + 8
+    assert C.sizeof(capi.MemeticParams) == 4 + 4 + 8 * 5 + 24 + 8
+    assert C.sizeof(capi.RunResult) == 8 * 4 + 8 * 5 + 8 + 8
     assert C.sizeof(capi.MemeticRecord) == 24

@@ -1,0 +1,19 @@
+"""The C++ labsolve:: drop-in (include/labsolve/*.hpp over the B200 library),
+exercised by tests/cpp/test_labsolve.cpp the way the reference's own doctest
+suites exercise the reference headers."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+BIN = os.path.join(ROOT, "tests", "cpp", "test_labsolve")
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_suite():
+    assert os.path.exists(BIN), "build with __graft_entry__.build() (make -C tests/cpp)"
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr
+    assert "0 failed" in r.stdout
