@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "liblabs_b200.so")
+LIB_PATH = os.environ.get("LABS_LIB_PATH") or os.path.join(HERE, "lib", "liblabs_b200.so")
 
 LABS_OK = 0
 LABS_ERR_INVALID_ARGUMENT = 1
@@ -431,6 +431,9 @@ class Solver:
 
     def request_stop(self):
         _check(self.L.labs_solver_request_stop(self.h))
+
+    def sync(self):
+        self.ctx.synchronize()
 
     def status(self):
         run, be, br = C.c_int32(0), C.c_int64(0), C.c_int32(0)

@@ -25,15 +25,22 @@ constexpr int kWarps = 4;  // walkers per block
 
 // Occupancy target: 8 blocks (32 warps) per SM up to n = 128 caps registers
 // at 64/thread; longer sequences carry twice the per-slot state.
+#ifndef LABS_MINB_SMALL
+#define LABS_MINB_SMALL 6
+#endif
+#ifndef LABS_MINB_LARGE
+#define LABS_MINB_LARGE 4
+#endif
 template <int NS>
 __host__ __device__ constexpr int min_blocks() {
-  return NS <= 4 ? 8 : 4;
+  return NS <= 4 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
 }
 
 template <int NS, bool MT>
 struct WarpSlot {
+  uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
+  uint64_t out[MT ? kMtN : 1];   // tempered outputs of the current block
   WalkSmem<NS> walk;
-  uint64_t mt[MT ? kMtN : 1];
 };
 
 template <int NS, bool MT>
@@ -53,11 +60,13 @@ __device__ __forceinline__ int global_warp() {
 }
 __device__ __forceinline__ int total_warps() { return gridDim.x * kWarps; }
 
-__device__ __forceinline__ void mt_load(uint64_t* s, const labs_rng_state& g,
-                                        int& idx) {
+// Load an engine state into the warp's slot and bind `rng` to it.
+__device__ __forceinline__ void mt_load(uint64_t* s, uint64_t* out, const labs_rng_state& g,
+                                        MtRng& rng) {
   for (int i = lane_id(); i < kMtN; i += 32) s[i] = g.mt[i];
-  idx = g.idx;
   __syncwarp();
+  mt_temper_all(s, out);
+  rng.bind(s, out, g.idx);
 }
 __device__ __forceinline__ void mt_store(const uint64_t* s, labs_rng_state& g,
                                          int idx) {
@@ -88,7 +97,7 @@ k_build(int n, int count, const uint64_t* __restrict__ words,
       const int j = 32 * b + lane_id();
       if (j < n && nbr) nbr[static_cast<size_t>(item) * n + j] = w.E + dE[b];
       if (j >= 1 && j < n && corr)
-        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.ck[b];
+        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.CK[b];
     }
     if (lane_id() == 0) energy[item] = w.E;
     __syncwarp();
@@ -145,8 +154,7 @@ k_scan(int n, int count, const uint64_t* __restrict__ words,
   const int nw = (n + 63) / 64;
   for (int item = global_warp(); item < count; item += total_warps()) {
     MtRng rng;
-    rng.mt = sl.mt;
-    mt_load(sl.mt, rng_states[item], rng.idx);
+    mt_load(sl.mt, sl.out, rng_states[item], rng);
     uint32_t in[NS];
     load_chunks<NS>(words + static_cast<size_t>(item) * nw, nw, in);
     w.init(n, in);
@@ -215,8 +223,7 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_tabu(WalkArgs
     int bestE = 0;
     if constexpr (MT) {
       MtRng rng;
-      rng.mt = sl.mt;
-      mt_load(sl.mt, A.mt[item], rng.idx);
+      mt_load(sl.mt, sl.out, A.mt[item], rng);
       for (int k = 0; k < A.walks; ++k) {
         int steps = 0;
         bestE = tabu_walk<NS>(w, n, cur, rng, A.cfg, best,
@@ -280,8 +287,7 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_memetic(Memet
     if (A.initialized[r] && A.status[r] != kRunning) continue;
     if constexpr (MT) {
       MtRng rng;
-      rng.mt = sl.mt;
-      mt_load(sl.mt, A.mt[r], rng.idx);
+      mt_load(sl.mt, sl.out, A.mt[r], rng);
       memetic_replica<NS>(A, r, w, rng);
       mt_store(sl.mt, A.mt[r], rng.idx);
     } else {

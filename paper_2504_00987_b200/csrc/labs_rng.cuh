@@ -49,57 +49,92 @@ __device__ __forceinline__ double u01_from_bits(uint64_t x) {
 // ---------------------------------------------------------------- MtRng --
 // State layout matches labs_rng_state (include/labs_b200.h): 312 words plus
 // the index of the next output; idx == 312 means "twist before next draw",
-// which is what a freshly seeded engine holds.
-struct MtRng {
-  uint64_t* mt;  // shared memory, 312 words, private to this warp
-  int idx;       // warp-uniform
+// which is what a freshly seeded engine holds. Alongside the raw state the
+// warp keeps the tempered outputs of the current block (`out`), produced by
+// the twist, so a draw is one shared load.
 
-  // Warp-cooperative twist. Reads of "old" words happen before any lane
-  // overwrites them (syncwarp between the read and write half of a chunk).
-  // Out of line: it runs once per 312 draws and would otherwise be inlined
-  // at every draw site.
-  __device__ __noinline__ void twist() {
-    const int lane = lane_id();
-    // i in [0, 156): inputs mt[i], mt[i+1], mt[i+156], all old.
+// Warp-cooperative twist: regenerates mt[0..312) and tempers the new block
+// into out[0..312). Reads of "old" words happen before any lane overwrites
+// them (syncwarp between the read and write half of each chunk). Out of line
+// and pointer-only so the caller's index stays in a register.
+__device__ __forceinline__ uint64_t lds_u64(uint32_t saddr) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u64(uint32_t saddr, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(saddr), "l"(v) : "memory");
+}
+
+__device__ __noinline__ void mt_twist(uint32_t mt, uint32_t out) {
+  const int lane = lane_id();
+  // i in [0, 156): inputs mt[i], mt[i+1], mt[i+156], all old.
 #pragma unroll 1
-    for (int base = 0; base < kMtN - kMtM; base += 32) {
-      int i = base + lane;
-      uint64_t v = 0;
-      if (i < kMtN - kMtM) v = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
-      __syncwarp();
-      if (i < kMtN - kMtM) mt[i] = v;
-      __syncwarp();
-    }
-    // i in [156, 311): inputs mt[i], mt[i+1] old, mt[i-156] new.
-#pragma unroll 1
-    for (int base = kMtN - kMtM; base < kMtN - 1; base += 32) {
-      int i = base + lane;
-      uint64_t v = 0;
-      if (i < kMtN - 1) v = mt_mix(mt[i], mt[i + 1], mt[i - (kMtN - kMtM)]);
-      __syncwarp();
-      if (i < kMtN - 1) mt[i] = v;
-      __syncwarp();
-    }
-    if (lane == 0) mt[kMtN - 1] = mt_mix(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
+  for (int base = 0; base < kMtN - kMtM; base += 32) {
+    const uint32_t i = base + lane;
+    uint64_t v = 0;
+    if (i < kMtN - kMtM)
+      v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)), lds_u64(mt + 8 * (i + kMtM)));
     __syncwarp();
-    idx = 0;
+    if (i < kMtN - kMtM) sts_u64(mt + 8 * i, v);
+    __syncwarp();
   }
+  // i in [156, 311): inputs mt[i], mt[i+1] old, mt[i-156] new.
+#pragma unroll 1
+  for (int base = kMtN - kMtM; base < kMtN - 1; base += 32) {
+    const uint32_t i = base + lane;
+    uint64_t v = 0;
+    if (i < kMtN - 1)
+      v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)),
+                 lds_u64(mt + 8 * (i - (kMtN - kMtM))));
+    __syncwarp();
+    if (i < kMtN - 1) sts_u64(mt + 8 * i, v);
+    __syncwarp();
+  }
+  if (lane == 0)
+    sts_u64(mt + 8 * (kMtN - 1),
+            mt_mix(lds_u64(mt + 8 * (kMtN - 1)), lds_u64(mt), lds_u64(mt + 8 * (kMtM - 1))));
+  __syncwarp();
+  for (int i = lane; i < kMtN; i += 32) sts_u64(out + 8 * i, mt_temper(lds_u64(mt + 8 * i)));
+  __syncwarp();
+}
 
+// Temper the current block without advancing (after loading a state).
+__device__ __forceinline__ void mt_temper_all(const uint64_t* mt, uint64_t* out) {
+  for (int i = lane_id(); i < kMtN; i += 32) out[i] = mt_temper(mt[i]);
+  __syncwarp();
+}
+
+struct MtRng {
+  uint32_t mt_s;   // shared-window address of the raw engine state
+  uint32_t out_s;  // shared-window address of the tempered block
+  int idx;         // warp-uniform
+
+  __device__ __forceinline__ void bind(uint64_t* raw, uint64_t* tempered, int i) {
+    mt_s = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+    out_s = static_cast<uint32_t>(__cvta_generic_to_shared(tempered));
+    idx = i;
+  }
   __device__ __forceinline__ uint64_t next() {
-    if (idx >= kMtN) twist();
-    uint64_t y = mt[idx];
+    if (idx >= kMtN) {
+      mt_twist(mt_s, out_s);
+      idx = 0;
+    }
+    const uint64_t v = lds_u64(out_s + 8u * static_cast<uint32_t>(idx));
     ++idx;
-    return mt_temper(y);
+    return v;
   }
-
   // Bulk: lane i (< count) receives draw i of the next `count` draws, with
   // count <= 32 and not crossing a twist (callers chunk on room()).
   __device__ __forceinline__ int room() {
-    if (idx >= kMtN) twist();
+    if (idx >= kMtN) {
+      mt_twist(mt_s, out_s);
+      idx = 0;
+    }
     return kMtN - idx;
   }
   __device__ __forceinline__ uint64_t peek_lane(int i) const {
-    return mt_temper(mt[idx + i]);
+    return lds_u64(out_s + 8u * static_cast<uint32_t>(idx + i));
   }
   __device__ __forceinline__ void advance(int count) { idx += count; }
 };
@@ -171,6 +206,24 @@ __device__ __forceinline__ long long uniform_int(R& rng, long long lo,
   const uint64_t range =
       static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo) + 1ULL;
   uint64_t x = rng.next();
+  if (range >> 32 == 0) {
+    // 64 x 32-bit product in two wide multiplies: low 64 bits and the
+    // high word (the result), same arithmetic as the 128-bit product.
+    const uint32_t r32 = static_cast<uint32_t>(range);
+    uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+    uint64_t p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+    if (static_cast<uint32_t>(p1) == 0 && static_cast<uint32_t>(p0) < r32) {
+      const uint64_t thr = (0ULL - range) % range;
+      uint64_t low = (p1 << 32) | static_cast<uint32_t>(p0);
+      while (low < thr) {
+        x = rng.next();
+        p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+        p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+        low = (p1 << 32) | static_cast<uint32_t>(p0);
+      }
+    }
+    return static_cast<long long>(static_cast<uint64_t>(lo) + (p1 >> 32));
+  }
   uint64_t low = x * range;
   if (low < range) {
     const uint64_t thr = (0ULL - range) % range;

@@ -19,15 +19,19 @@
 // and h_p -= 2 sigma (n - 2 + Q_{2p}); E += dE_p. All right-hand sides use the
 // pre-flip vectors; s_x = 0 outside [0, n). Everything is exact int32
 // arithmetic, so dE_j is bit-identical to the reference's neighbor_energy(j)
-// - E (derivation and the randomized proof-by-test: DESIGN.md §3,
-// tests/test_oracle_cpu.py::test_incremental_identities).
+// - E (derivation: DESIGN.md §3; randomized proof-by-test:
+// tests/test_oracle_cpu.py::test_incremental_identities; device parity:
+// tests/test_parity_gpu.py).
 //
-// Layout: h, Q_{2j}, s_j, expiry and C_j stay in registers (one per slot);
-// C and Q also live in shared memory for the two lane-varying gathers
-// C_{|j-p|} and Q_{p+j}; spins live in a zero-padded int8 shared array so
-// s_x for any x in [-L, 2L) is one LDS with the range check folded into the
-// padding. The tabu list is the per-slot `ex` register: admissible iff
-// ex < t (proj/src/tabu.cpp:43-47).
+// Register layout per slot (pre-scaled so each tabu step is a few IMADs):
+//   H = 4 h_j, HQ = 4 (n - 2 + Q_{2j}), MS = -s_j, EX = expiry, CK = C_j
+//   => dE_j = HQ + MS * H (one IMAD).
+// Shared layout per warp: C mirrored as C2[L + d] = C_{|d|} so the gather
+// C_{|j-p|} is one LDS at a per-step base + 128 b; Q[m]; spins as a
+// zero-padded int8 array S[L + x] so s_x for any x in (-L, 2L) is one LDS
+// with the range check folded into the padding. Invalid lanes (j >= n) keep
+// EX = INT_MAX (never admissible) and s_j = 0, which makes every update they
+// perform a no-op on the entries valid lanes read.
 #pragma once
 #include <climits>
 #include <cstdint>
@@ -39,7 +43,7 @@ namespace labsk {
 template <int NS>
 struct WalkSmem {
   static constexpr int L = 32 * NS;
-  int32_t C[L];                // C[k], k in [1, n); C[0] and k >= n hold 0
+  int32_t C2[2 * L];           // C2[L + d] = C_{|d|}, d in (-L, L)
   int32_t Q[2 * L];            // Q[m], m in [0, 2n-1)
   uint32_t B32[3 * NS + 2];    // bits of s; position x at word (x + L) >> 5
   uint32_t R32[3 * NS + 2];    // bits of reversed s (R_x = s_{n-1-x})
@@ -90,24 +94,22 @@ struct Walker {
   static constexpr int L = 32 * NS;
   WalkSmem<NS>* sm;
   int n;
-  // per-slot registers (candidate j = 32*b + lane)
-  int h[NS], q[NS], sp[NS], ex[NS], ck[NS];
+  int H[NS], HQ[NS], MS[NS], EX[NS], CK[NS];
   int E;
-
-  __device__ __forceinline__ int lane() const { return lane_id(); }
 
   // Build C, Q, h, E from `in` (chunks of 32 positions, padding zero).
   __device__ __forceinline__ void init(int n_, const uint32_t (&in)[NS]) {
     n = n_;
-    const int ln = lane();
+    const int ln = lane_id();
     WalkSmem<NS>& s = *sm;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = 32 * b + ln;
       const int bit = ((in[b] & lowmask(n - 32 * b)) >> ln) & 1u;
-      sp[b] = j < n ? 1 - 2 * bit : 0;
-      s.S[L + j] = static_cast<int8_t>(sp[b]);
-      ex[b] = 0;
+      const int sp = j < n ? 1 - 2 * bit : 0;
+      MS[b] = -sp;
+      s.S[L + j] = static_cast<int8_t>(sp);
+      EX[b] = j < n ? 0 : INT_MAX;
     }
     if (ln == 0) {
 #pragma unroll
@@ -139,8 +141,9 @@ struct Walker {
         }
         c = len - 2 * acc;
       }
-      ck[b] = c;
-      s.C[k] = c;
+      CK[b] = c;
+      s.C2[L + k] = c;
+      s.C2[L - k] = c;
       e2 += c * c;
     }
     E = __reduce_add_sync(kFull, e2);
@@ -155,8 +158,7 @@ struct Walker {
         int acc = 0;
 #pragma unroll
         for (int cc = 0; cc < NS; ++cc) {
-          const uint32_t vm =
-              lowmask(hi - 32 * cc + 1) & ~lowmask(lo - 32 * cc);
+          const uint32_t vm = lowmask(hi - 32 * cc + 1) & ~lowmask(lo - 32 * cc);
           if (vm) {
             const uint32_t x = window32<NS>(s.R32, n - 1 - m + 32 * cc);
             acc += __popc((s.B32[NS + cc] ^ x) & vm);
@@ -167,79 +169,86 @@ struct Walker {
       s.Q[m] = qv;
     }
     __syncwarp();
+    int h[NS];
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = 32 * b + ln;
-      q[b] = s.Q[2 * j];
+      HQ[b] = 4 * (n - 2 + s.Q[2 * j]);
       h[b] = 0;
     }
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
 #pragma unroll 2
     for (int k = 1; k < n; ++k) {
-      const int c = s.C[k];
+      const int c = s.C2[L + k];
 #pragma unroll
       for (int b = 0; b < NS; ++b) {
         const int j = 32 * b + ln;
-        h[b] += c * (static_cast<int>(s.S[L + j + k]) +
-                     static_cast<int>(s.S[L + j - k]));
+        h[b] += c * (static_cast<int>(s.S[L + j + k]) + static_cast<int>(s.S[L + j - k]));
       }
     }
+#pragma unroll
+    for (int b = 0; b < NS; ++b) H[b] = 4 * h[b];
   }
 
   // dE_j for every slot.
   __device__ __forceinline__ void delta(int (&dE)[NS]) const {
 #pragma unroll
-    for (int b = 0; b < NS; ++b) dE[b] = 4 * (n - 2 + q[b] - sp[b] * h[b]);
+    for (int b = 0; b < NS; ++b) dE[b] = HQ[b] + MS[b] * H[b];
   }
 
-  // Commit flip `pos` (warp-uniform). Expiry of pos becomes t + tenure.
-  // Phase A updates registers slot by slot from pre-flip shared values; the
-  // only cross-lane hazards (C[j] and S[pos] read by other lanes) are written
-  // in phase B after a warp barrier. Q[pos+j] is read and written by lane j
-  // alone, so it is updated in place during phase A.
+  // Commit flip `pos` (warp-uniform); its expiry becomes t + tenure.
+  // Phase A reads pre-flip shared values and updates registers and Q[pos+j]
+  // (read and written by lane j alone); phase B, after a warp barrier,
+  // publishes C_j (mirrored) and the flipped spin, which other lanes read.
   __device__ __forceinline__ void apply(int pos, int dEp, int t, int tenure) {
-    const int ln = lane();
+    const int ln = lane_id();
     WalkSmem<NS>& s = *sm;
     const int sig = s.S[L + pos];
-    const int sig2 = 2 * sig, sig4 = 4 * sig;
+    const int c16 = sig * -16, c8 = sig * -8, c4 = sig * -4, c2 = sig * -2;
+    const int32_t* cgp = &s.C2[L + ln - pos];
+    int32_t* qp = &s.Q[pos + ln];
+    const int8_t* s1p = &s.S[L + 2 * pos - ln];
+    const int8_t* s2p = &s.S[L + 2 * ln - pos];
+    const int8_t* smp = &s.S[L + pos - ln];
+    const int8_t* spp = &s.S[L + pos + ln];
+    const int exp_new = t + tenure;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + ln;
-      const int d = j - pos;
-      const int cg = s.C[d < 0 ? -d : d];
-      const int qg = s.Q[pos + j];
-      const int s1 = s.S[L + 2 * pos - j];
-      const int s2 = s.S[L + 2 * j - pos];
-      const int sm_ = s.S[L + pos - j];
-      const int spl = s.S[L + pos + j];
-      if (j < n) {
-        if (j != pos) {
-          h[b] += 4 * s1 + 8 * sp[b] - sig4 * cg - sig2 * qg;
-          s.Q[pos + j] = qg - sig4 * sp[b];
-          q[b] -= sig4 * s2;
-        } else {
-          h[b] -= sig2 * (n - 2 + q[b]);
-          sp[b] = -sp[b];
-          ex[b] = t + tenure;
-        }
-        if (j >= 1) ck[b] -= sig2 * (sm_ + spl);
+      const bool isp = 32 * b + ln == pos;
+      const int cg = cgp[32 * b];
+      const int qg = qp[32 * b];
+      const int s1 = s1p[-32 * b];
+      const int s2 = s2p[64 * b];
+      const int smv = smp[-32 * b];
+      const int spv = spp[32 * b];
+      // j != p: H += 16 s_{2p-j} + 32 s_j + c16 C_{|j-p|} + c8 Q_{p+j}
+      const int hn = H[b] + 16 * s1 - 32 * MS[b] + c16 * cg + c8 * qg;
+      const int hp = H[b] + c2 * HQ[b];  // j == p: H -= 8 sigma (n-2+Q_2p)
+      H[b] = isp ? hp : hn;
+      if (!isp) {
+        qp[32 * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
+        HQ[b] += c16 * s2;             // Q_{2j}  -= 4 sigma s_{2j-p}
       }
+      CK[b] += c2 * (smv + spv);       // C_j -= 2 sigma (s_{p-j} + s_{p+j})
+      MS[b] = isp ? -MS[b] : MS[b];
+      EX[b] = isp ? exp_new : EX[b];
     }
     __syncwarp();
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = 32 * b + ln;
-      if (j >= 1 && j < n) s.C[j] = ck[b];
-      if (j == pos) s.S[L + pos] = static_cast<int8_t>(-sig);
+      s.C2[L + j] = CK[b];
+      s.C2[L - j] = CK[b];
     }
+    s.S[L + pos] = static_cast<int8_t>(-sig);  // every lane stores the same byte
     E += dEp;
     __syncwarp();
   }
 
-  // Current sequence as 32-bit chunks (bit 1 = spin -1), from the spins.
+  // Current sequence as 32-bit chunks (bit 1 = spin -1).
   __device__ __forceinline__ void chunks(uint32_t (&out)[NS]) const {
 #pragma unroll
-    for (int b = 0; b < NS; ++b) out[b] = __ballot_sync(kFull, sp[b] < 0);
+    for (int b = 0; b < NS; ++b) out[b] = __ballot_sync(kFull, MS[b] > 0);
   }
 };
 
@@ -272,18 +281,20 @@ __device__ __forceinline__ int nth_hit(const bool (&hit)[NS],
 
 // Select the move at iteration t: admissible argmin with the tie/fallback
 // semantics of scan_neighborhood (proj/src/correlation_state.cpp:141-165).
-// adm_ext: optional external admissibility (one bit per slot per lane).
+// Keys pack dE * 256 + j, so one warp min yields the minimum and its lowest
+// position (|dE| < 2^22 and j < 256 for n <= 256).
 template <int NS, class R>
 __device__ __forceinline__ void select_move(const int (&dE)[NS],
                                             const bool (&adm)[NS], int n,
                                             int tie_rule, R& rng, int& pos,
                                             int& dEp, int& fallback,
                                             uint32_t (&msk)[NS], int& ntie) {
+  const int ln = lane_id();
   int key[NS];
   int kmin = INT_MAX;
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
-    key[b] = adm[b] ? dE[b] : INT_MAX;
+    key[b] = adm[b] ? dE[b] * 256 + 32 * b + ln : INT_MAX;
     kmin = min(kmin, key[b]);
   }
   kmin = __reduce_min_sync(kFull, kmin);
@@ -296,19 +307,21 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
     for (int b = 0; b < NS; ++b) msk[b] = 0u;
     return;
   }
-  int cnt = 0;
+  const int dmin = kmin >> 8;
   bool hit[NS];
+  int cnt = 0;
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
-    hit[b] = key[b] == kmin;
+    hit[b] = (key[b] >> 8) == dmin;
     msk[b] = __ballot_sync(kFull, hit[b]);
     cnt += __popc(msk[b]);
   }
-  int r = 0;
-  if (cnt > 1 && tie_rule == 0)
-    r = static_cast<int>(uniform_int(rng, 0, static_cast<long long>(cnt) - 1));
-  pos = nth_hit<NS>(hit, msk, r);
-  dEp = kmin;
+  pos = kmin & 255;
+  if (cnt > 1 && tie_rule == 0) {
+    const int r = static_cast<int>(uniform_int(rng, 0, static_cast<long long>(cnt) - 1));
+    if (r) pos = nth_hit<NS>(hit, msk, r);
+  }
+  dEp = dmin;
   fallback = 0;
   ntie = cnt;
 }
@@ -336,20 +349,22 @@ __device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n,
   }
   w.init(n, in);
   int bestE = w.E;
+  const bool asp = cfg.aspiration != 0;
+  const int tie_rule = cfg.tie_rule;
 #pragma unroll
   for (int b = 0; b < NS; ++b) best[b] = in[b] & lowmask(n - 32 * b);
   for (int t = 1; t <= m; ++t) {
     int dE[NS];
     bool adm[NS];
     w.delta(dE);
+    // aspiration: a tabu move is admissible if it lands strictly below the
+    // walk's best (off in reference mode: thr = INT_MIN never passes).
+    const int thr = asp ? bestE - w.E : INT_MIN;
 #pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + lane_id();
-      adm[b] = j < n && (w.ex[b] < t || (cfg.aspiration && w.E + dE[b] < bestE));
-    }
+    for (int b = 0; b < NS; ++b) adm[b] = (w.EX[b] < t) | (dE[b] < thr);
     int pos, dEp, fb, ntie;
     uint32_t msk[NS];
-    select_move<NS>(dE, adm, n, cfg.tie_rule, rng, pos, dEp, fb, msk, ntie);
+    select_move<NS>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
     const int tenure = static_cast<int>(uniform_int(rng, min_t, max_t));
     w.apply(pos, dEp, t, tenure);
     if (w.E < bestE) {
