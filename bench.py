@@ -246,11 +246,14 @@ def main():
     # roofline: the memetic kernel is the step (one launch per step)
     peak_gops = ctx.int_peak_gops()
     achieved_gops = per_gpu * OPS_PER_FLIP_EVAL / 1e9
+    # DRAM bytes per launch from the committed ncu capture, scaled to this
+    # run's epoch length (the kernel's traffic is per memetic iteration).
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"k_memetic_n{n}_per_launch_bytes")
+            per_ms = json.load(open(prof)).get(f"k_memetic_n{n}_dram_bytes_per_ms")
+            traffic = per_ms * (time_ms / args.steps) if per_ms else None
         except Exception:
             traffic = None
 

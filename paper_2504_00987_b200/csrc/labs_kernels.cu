@@ -23,8 +23,11 @@ namespace labsk {
 
 constexpr int kWarps = 4;  // walkers per block
 
-// Occupancy target: 8 blocks (32 warps) per SM up to n = 128 caps registers
-// at 64/thread; longer sequences carry twice the per-slot state.
+// Occupancy target. The walker is issue-bound (ncu: ~89% issue slots busy),
+// so registers matter more than warps: 6 blocks (24 warps) per SM up to
+// n = 128 caps registers at 85/thread, which removed the smem-base
+// rematerialization of the 64-register build (+7% at n=64, +12% at n=119,
+// measured); longer sequences carry twice the per-slot state.
 #ifndef LABS_MINB_SMALL
 #define LABS_MINB_SMALL 6
 #endif
