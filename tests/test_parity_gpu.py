@@ -252,3 +252,15 @@ def test_validation_errors(ctx):
         ctx.run_replicas(12, 3, 1, capi.memetic_params(population_size=1))
     with pytest.raises(ValueError):
         ctx.build_state(3, [[0b1000]])  # nonzero padding bit
+
+
+def test_readme_solve_example(ctx):
+    """README.md:110-117: `labs solve --n 20 --target 26 --replicas 2 --seed 42`
+    -> replica 1 (seed 43) wins with E=26 after 98 iterations, best C9EF5."""
+    from paper_2504_00987_b200.sequence import encode_hex
+    best, per = ctx.run_replicas(20, 2, 42, capi.memetic_params(target_energy=26,
+                                                                max_seconds=30.0))
+    assert best["reached_target"] and best["best_energy"] == 26
+    r1 = per[1]
+    assert r1["reached_target"] and r1["iterations"] == 98
+    assert encode_hex(r1["best"], 20) == "C9EF5"
