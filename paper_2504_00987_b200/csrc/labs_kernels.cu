@@ -177,7 +177,7 @@ k_scan(int n, int count, const uint64_t* __restrict__ words,
 #pragma unroll
     for (int b = 0; b < NS; ++b) msk[b] = 0u;
     if (any || allow_fallback)
-      select_move<NS>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
+      select_move<NS, true>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
     if (lane_id() == 0) {
       pos_out[item] = pos;
       e_out[item] = pos >= 0 ? static_cast<int64_t>(w.E) + dEp : 0;

@@ -72,11 +72,8 @@ template <int NS>
 __device__ __forceinline__ int energy_of(WalkSmem<NS>& s, int n,
                                          const uint32_t (&c)[NS]) {
   const int ln = lane_id();
-  if (ln == 0) {
-#pragma unroll
-    for (int b = 0; b < NS; ++b) s.B32[NS + b] = c[b] & lowmask(n - 32 * b);
-  }
-  __syncwarp();
+  s.put_bits(n, c);
+  const uint32_t* B32 = s.B32();
   int e2 = 0;
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
@@ -86,8 +83,8 @@ __device__ __forceinline__ int energy_of(WalkSmem<NS>& s, int n,
       int acc = 0;
 #pragma unroll
       for (int cc = 0; cc < NS; ++cc) {
-        const uint32_t a = s.B32[NS + cc];
-        const uint32_t x = window32<NS>(s.B32, 32 * cc + k);
+        const uint32_t a = B32[NS + cc];
+        const uint32_t x = window32<NS>(B32, 32 * cc + k);
         acc += __popc((a ^ x) & lowmask(len - 32 * cc));
       }
       const int cv = len - 2 * acc;

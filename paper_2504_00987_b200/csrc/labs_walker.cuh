@@ -27,43 +27,62 @@
 //   H = 4 h_j, HQ = 4 (n - 2 + Q_{2j}), MS = -s_j, EX = expiry, CK = C_j
 //   => dE_j = HQ + MS * H (one IMAD).
 // Shared layout per warp: C mirrored as C2[L + d] = C_{|d|} so the gather
-// C_{|j-p|} is one LDS at a per-step base + 128 b; Q[m]; spins as a
-// zero-padded int8 array S[L + x] so s_x for any x in (-L, 2L) is one LDS
-// with the range check folded into the padding. Invalid lanes (j >= n) keep
-// EX = INT_MAX (never admissible) and s_j = 0, which makes every update they
-// perform a no-op on the entries valid lanes read.
+// C_{|j-p|} is one LDS at a per-step base + 128 b, double-buffered (a step
+// reads one buffer and writes the other); Q[m]; spins as a zero-padded int8
+// array S[L + x] so s_x for any x in (-L, 2L) is one LDS with the range check
+// folded into the padding. The flipped spin is stored by every lane at the
+// start of the next step (each lane then reads its own store), so a tabu
+// step needs a single warp barrier. Invalid lanes (j >= n) keep EX = INT_MAX
+// (never admissible) and s_j = 0, which makes every update they perform a
+// no-op on the entries valid lanes read.
 #pragma once
 #include <climits>
 #include <cstdint>
 
 #include "labs_rng.cuh"
 
+#ifndef LABS_TIE_DUAL
+#define LABS_TIE_DUAL 0
+#endif
+
 namespace labsk {
+
+__device__ __forceinline__ uint32_t lowmask(int x);
 
 template <int NS>
 struct WalkSmem {
   static constexpr int L = 32 * NS;
-  int32_t C2[2 * L];           // C2[L + d] = C_{|d|}, d in (-L, L)
+  int32_t C2[2][2 * L];        // C2[buf][L + d] = C_{|d|}, d in (-L, L); 2 buffers
   int32_t Q[2 * L];            // Q[m], m in [0, 2n-1)
-  uint32_t B32[3 * NS + 2];    // bits of s; position x at word (x + L) >> 5
-  uint32_t R32[3 * NS + 2];    // bits of reversed s (R_x = s_{n-1-x})
   int8_t S[3 * L];             // spins (+1/-1), S[L + x]; 0 outside [0, n)
-};
-
-// Zero the padding once per kernel; positions [0, n) are rewritten per walk.
-template <int NS>
-__device__ __forceinline__ void smem_clear(WalkSmem<NS>& sm) {
-  const int lane = lane_id();
-  for (int i = lane; i < 3 * NS + 2; i += 32) {
-    sm.B32[i] = 0u;
-    sm.R32[i] = 0u;
+  // Packed bit windows for the O(n^2/32) popcount build, aliased onto the
+  // second C buffer (idle until the walk's first step): B32 holds s
+  // (position x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
+  static constexpr int kBitWords = 3 * NS + 2;
+  static_assert(2 * kBitWords <= 2 * L, "bit windows must fit one C buffer");
+  __device__ __forceinline__ uint32_t* B32() { return reinterpret_cast<uint32_t*>(C2[1]); }
+  __device__ __forceinline__ uint32_t* R32() { return B32() + kBitWords; }
+  // Zero both windows and store the payload chunks of s.
+  __device__ __forceinline__ void put_bits(int n, const uint32_t* in) {
+    uint32_t* b = B32();
+    for (int i = lane_id(); i < 2 * kBitWords; i += 32) b[i] = 0u;
+    __syncwarp();
+    if (lane_id() == 0)
+      for (int c = 0; c < NS; ++c) b[NS + c] = in[c] & lowmask(n - 32 * c);
+    __syncwarp();
   }
-  for (int i = lane; i < 3 * 32 * NS; i += 32) sm.S[i] = 0;
-  __syncwarp();
-}
+};
 
 __device__ __forceinline__ uint32_t lowmask(int x) {
   return x <= 0 ? 0u : (x >= 32 ? kFull : ((1u << x) - 1u));
+}
+
+// Zero the spin padding once per kernel; positions [0, n) are rewritten per
+// walk.
+template <int NS>
+__device__ __forceinline__ void smem_clear(WalkSmem<NS>& sm) {
+  for (int i = lane_id(); i < 3 * 32 * NS; i += 32) sm.S[i] = 0;
+  __syncwarp();
 }
 
 // Bits [o, o+32) of a zero-padded packed array (positions [-L, 2L+32)).
@@ -96,6 +115,9 @@ struct Walker {
   int n;
   int H[NS], HQ[NS], MS[NS], EX[NS], CK[NS];
   int E;
+  int cb;        // C2 buffer holding the current C
+  int pend_pos;  // flipped position whose spin store is pending (-1: none)
+  int pend_val;
 
   // Build C, Q, h, E from `in` (chunks of 32 positions, padding zero).
   __device__ __forceinline__ void init(int n_, const uint32_t (&in)[NS]) {
@@ -111,17 +133,15 @@ struct Walker {
       s.S[L + j] = static_cast<int8_t>(sp);
       EX[b] = j < n ? 0 : INT_MAX;
     }
-    if (ln == 0) {
-#pragma unroll
-      for (int b = 0; b < NS; ++b) s.B32[NS + b] = in[b] & lowmask(n - 32 * b);
-    }
-    __syncwarp();
+    s.put_bits(n, in);
+    uint32_t* B32 = s.B32();
+    uint32_t* R32 = s.R32();
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int i = 32 * b + ln;
       const bool rb = i < n && s.S[L + n - 1 - i] < 0;
       const uint32_t m = __ballot_sync(kFull, rb);
-      if (ln == 0) s.R32[NS + b] = m;
+      if (ln == 0) R32[NS + b] = m;
     }
     __syncwarp();
     // C_k = (n-k) - 2 popc(s xor (s >> k)) over the n-k valid pairs.
@@ -135,18 +155,21 @@ struct Walker {
         int acc = 0;
 #pragma unroll
         for (int cc = 0; cc < NS; ++cc) {
-          const uint32_t a = s.B32[NS + cc];
-          const uint32_t x = window32<NS>(s.B32, 32 * cc + k);
+          const uint32_t a = B32[NS + cc];
+          const uint32_t x = window32<NS>(B32, 32 * cc + k);
           acc += __popc((a ^ x) & lowmask(len - 32 * cc));
         }
         c = len - 2 * acc;
       }
       CK[b] = c;
-      s.C2[L + k] = c;
-      s.C2[L - k] = c;
+      s.C2[0][L + k] = c;
+      s.C2[0][L - k] = c;
       e2 += c * c;
     }
     E = __reduce_add_sync(kFull, e2);
+    cb = 0;
+    pend_pos = -1;
+    pend_val = 0;
     // Q_m = sum_i s_i s_{m-i}: s against reversed s at offset n-1-m.
 #pragma unroll 1
     for (int a = 0; a < 2 * NS; ++a) {
@@ -160,8 +183,8 @@ struct Walker {
         for (int cc = 0; cc < NS; ++cc) {
           const uint32_t vm = lowmask(hi - 32 * cc + 1) & ~lowmask(lo - 32 * cc);
           if (vm) {
-            const uint32_t x = window32<NS>(s.R32, n - 1 - m + 32 * cc);
-            acc += __popc((s.B32[NS + cc] ^ x) & vm);
+            const uint32_t x = window32<NS>(R32, n - 1 - m + 32 * cc);
+            acc += __popc((B32[NS + cc] ^ x) & vm);
           }
         }
         qv = (hi - lo + 1) - 2 * acc;
@@ -179,7 +202,7 @@ struct Walker {
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
 #pragma unroll 2
     for (int k = 1; k < n; ++k) {
-      const int c = s.C2[L + k];
+      const int c = s.C2[0][L + k];
 #pragma unroll
       for (int b = 0; b < NS; ++b) {
         const int j = 32 * b + ln;
@@ -196,16 +219,24 @@ struct Walker {
     for (int b = 0; b < NS; ++b) dE[b] = HQ[b] + MS[b] * H[b];
   }
 
-  // Commit flip `pos` (warp-uniform); its expiry becomes t + tenure.
-  // Phase A reads pre-flip shared values and updates registers and Q[pos+j]
-  // (read and written by lane j alone); phase B, after a warp barrier,
-  // publishes C_j (mirrored) and the flipped spin, which other lanes read.
+  // Spin store of the previous flip, performed by every lane before it reads
+  // S (each lane then observes its own store).
+  __device__ __forceinline__ void flush_spin() {
+    if (pend_pos >= 0) sm->S[L + pend_pos] = static_cast<int8_t>(pend_val);
+  }
+
+  // Commit flip `pos` (warp-uniform); its expiry becomes t + tenure. Reads
+  // pre-flip values (C2[cb], Q, S) and writes C2[cb ^ 1] and Q[pos + j] (read
+  // and written by lane j alone); one warp barrier orders this step's stores
+  // before the next step's loads.
   __device__ __forceinline__ void apply(int pos, int dEp, int t, int tenure) {
     const int ln = lane_id();
     WalkSmem<NS>& s = *sm;
+    flush_spin();
     const int sig = s.S[L + pos];
     const int c16 = sig * -16, c8 = sig * -8, c4 = sig * -4, c2 = sig * -2;
-    const int32_t* cgp = &s.C2[L + ln - pos];
+    const int32_t* cgp = &s.C2[cb][L + ln - pos];
+    int32_t* cw = &s.C2[cb ^ 1][L];
     int32_t* qp = &s.Q[pos + ln];
     const int8_t* s1p = &s.S[L + 2 * pos - ln];
     const int8_t* s2p = &s.S[L + 2 * ln - pos];
@@ -214,7 +245,8 @@ struct Walker {
     const int exp_new = t + tenure;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      const bool isp = 32 * b + ln == pos;
+      const int j = 32 * b + ln;
+      const bool isp = j == pos;
       const int cg = cgp[32 * b];
       const int qg = qp[32 * b];
       const int s1 = s1p[-32 * b];
@@ -230,17 +262,14 @@ struct Walker {
         HQ[b] += c16 * s2;             // Q_{2j}  -= 4 sigma s_{2j-p}
       }
       CK[b] += c2 * (smv + spv);       // C_j -= 2 sigma (s_{p-j} + s_{p+j})
+      cw[j] = CK[b];
+      cw[-j] = CK[b];
       MS[b] = isp ? -MS[b] : MS[b];
       EX[b] = isp ? exp_new : EX[b];
     }
-    __syncwarp();
-#pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + ln;
-      s.C2[L + j] = CK[b];
-      s.C2[L - j] = CK[b];
-    }
-    s.S[L + pos] = static_cast<int8_t>(-sig);  // every lane stores the same byte
+    cb ^= 1;
+    pend_pos = pos;
+    pend_val = -sig;
     E += dEp;
     __syncwarp();
   }
@@ -282,8 +311,10 @@ __device__ __forceinline__ int nth_hit(const bool (&hit)[NS],
 // Select the move at iteration t: admissible argmin with the tie/fallback
 // semantics of scan_neighborhood (proj/src/correlation_state.cpp:141-165).
 // Keys pack dE * 256 + j, so one warp min yields the minimum and its lowest
-// position (|dE| < 2^22 and j < 256 for n <= 256).
-template <int NS, class R>
+// position (|dE| < 2^22 and j < 256 for n <= 256). A second min over the
+// other keys detects whether the minimum is tied; the tie set (ballots) is
+// only built when it is (or when FULL_TIES asks for it).
+template <int NS, bool FULL_TIES, class R>
 __device__ __forceinline__ void select_move(const int (&dE)[NS],
                                             const bool (&adm)[NS], int n,
                                             int tie_rule, R& rng, int& pos,
@@ -292,12 +323,23 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
   const int ln = lane_id();
   int key[NS];
   int kmin = INT_MAX;
+#if LABS_TIE_DUAL
+  // Second key orders equal dE by descending position: its min is the
+  // highest tied position, reduced in parallel with the first.
+  int kmin_hi = INT_MAX;
+#endif
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
     key[b] = adm[b] ? dE[b] * 256 + 32 * b + ln : INT_MAX;
     kmin = min(kmin, key[b]);
+#if LABS_TIE_DUAL
+    kmin_hi = min(kmin_hi, adm[b] ? dE[b] * 256 + (255 - 32 * b - ln) : INT_MAX);
+#endif
   }
   kmin = __reduce_min_sync(kFull, kmin);
+#if LABS_TIE_DUAL
+  if (!FULL_TIES && tie_rule == 0) kmin_hi = __reduce_min_sync(kFull, kmin_hi);
+#endif
   if (kmin == INT_MAX) {
     pos = static_cast<int>(uniform_int(rng, 0, n - 1));
     dEp = at_position<NS>(dE, pos);
@@ -308,29 +350,44 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
     return;
   }
   const int dmin = kmin >> 8;
-  bool hit[NS];
-  int cnt = 0;
-#pragma unroll
-  for (int b = 0; b < NS; ++b) {
-    hit[b] = (key[b] >> 8) == dmin;
-    msk[b] = __ballot_sync(kFull, hit[b]);
-    cnt += __popc(msk[b]);
-  }
   pos = kmin & 255;
-  if (cnt > 1 && tie_rule == 0) {
-    const int r = static_cast<int>(uniform_int(rng, 0, static_cast<long long>(cnt) - 1));
-    if (r) pos = nth_hit<NS>(hit, msk, r);
-  }
   dEp = dmin;
   fallback = 0;
-  ntie = cnt;
+  bool tied = FULL_TIES;
+  if (!FULL_TIES && tie_rule == 0) {
+#if LABS_TIE_DUAL
+    tied = (255 - (kmin_hi & 255)) != pos;
+#else
+    int k2 = INT_MAX;
+#pragma unroll
+    for (int b = 0; b < NS; ++b) k2 = min(k2, key[b] == kmin ? INT_MAX : key[b]);
+    k2 = __reduce_min_sync(kFull, k2);
+    tied = (k2 >> 8) == dmin;
+#endif
+  }
+  ntie = 1;
+  if (tied) {
+    bool hit[NS];
+    int cnt = 0;
+#pragma unroll
+    for (int b = 0; b < NS; ++b) {
+      hit[b] = (key[b] >> 8) == dmin;
+      msk[b] = __ballot_sync(kFull, hit[b]);
+      cnt += __popc(msk[b]);
+    }
+    ntie = cnt;
+    if (cnt > 1 && tie_rule == 0) {
+      const int r = static_cast<int>(uniform_int(rng, 0, static_cast<long long>(cnt) - 1));
+      if (r) pos = nth_hit<NS>(hit, msk, r);
+    }
+  }
 }
 
 // tabu_search (proj/src/tabu.cpp:17-56) for one walker. `in` is the start
 // sequence; on return `best` holds the best visited sequence (the start
 // counts as visited) and the return value is its energy.
-template <int NS, class R>
-__device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n,
+template <int NS, bool ASP, class R>
+__device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
                                          const uint32_t (&in)[NS], R& rng,
                                          const TabuCfg& cfg,
                                          uint32_t (&best)[NS], int* info,
@@ -349,7 +406,6 @@ __device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n,
   }
   w.init(n, in);
   int bestE = w.E;
-  const bool asp = cfg.aspiration != 0;
   const int tie_rule = cfg.tie_rule;
 #pragma unroll
   for (int b = 0; b < NS; ++b) best[b] = in[b] & lowmask(n - 32 * b);
@@ -357,14 +413,19 @@ __device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n,
     int dE[NS];
     bool adm[NS];
     w.delta(dE);
-    // aspiration: a tabu move is admissible if it lands strictly below the
-    // walk's best (off in reference mode: thr = INT_MIN never passes).
-    const int thr = asp ? bestE - w.E : INT_MIN;
+    // aspiration (not in the reference): a tabu move is admissible if it
+    // lands strictly below the walk's best.
+    if (ASP) {
+      const int thr = bestE - w.E;
 #pragma unroll
-    for (int b = 0; b < NS; ++b) adm[b] = (w.EX[b] < t) | (dE[b] < thr);
+      for (int b = 0; b < NS; ++b) adm[b] = (w.EX[b] < t) | (dE[b] < thr);
+    } else {
+#pragma unroll
+      for (int b = 0; b < NS; ++b) adm[b] = w.EX[b] < t;
+    }
     int pos, dEp, fb, ntie;
     uint32_t msk[NS];
-    select_move<NS>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
+    select_move<NS, false>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
     const int tenure = static_cast<int>(uniform_int(rng, min_t, max_t));
     w.apply(pos, dEp, t, tenure);
     if (w.E < bestE) {
@@ -383,6 +444,15 @@ __device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n,
   }
   if (steps_out) *steps_out = m;
   return bestE;
+}
+
+template <int NS, class R>
+__device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n, const uint32_t (&in)[NS],
+                                         R& rng, const TabuCfg& cfg, uint32_t (&best)[NS],
+                                         int* info, StepRec* trace, int* steps_out) {
+  if (cfg.aspiration)
+    return tabu_walk_impl<NS, true>(w, n, in, rng, cfg, best, info, trace, steps_out);
+  return tabu_walk_impl<NS, false>(w, n, in, rng, cfg, best, info, trace, steps_out);
 }
 
 // u64 words (global layout) <-> 32-bit chunks (register layout).
