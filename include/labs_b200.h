@@ -266,6 +266,18 @@ int labs_solver_import_elites(labs_solver* s, int count,
                               const uint64_t* d_words,
                               const int64_t* d_energies, int rotation);
 
+/* ------------------------------------- K5: exhaustive ground truth ------ */
+/* Replaces brute_force_optimum / enumerate_local_optima
+ * (proj/include/labsolve/oracle.hpp:18-24; oracle.cpp:23-151) on the device:
+ * a Gray-code walk over the 2^(n-1) sequences with s_0 = +1, n <= 64 (the
+ * reference stops at 30 / 24). exhaustive_optimum returns the optimal energy
+ * and every optimal sequence of that half (raw, not canonicalized; up to cap,
+ * *count = how many exist). local_optima counts strict local optima of the
+ * whole space (x2 for the complement half, as the reference does). */
+int labs_exhaustive_optimum(labs_ctx* ctx, int n, int64_t* optimal_energy,
+                            uint64_t* witnesses, int64_t cap, int64_t* count);
+int labs_local_optima(labs_ctx* ctx, int n, int64_t* count);
+
 /* ------------------------------------------------------- diagnostics --- */
 /* Measured INT32 lane-instruction rate of this device (IMAD on the FMA pipe
  * alongside IADD3/LOP3 on the ALU pipe), in Gop/s: the roofline denominator

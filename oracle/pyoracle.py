@@ -259,6 +259,21 @@ class Reference:
         L.ref_tabu_throughput.argtypes = [C.c_int, C.c_int, C.c_double, i64p,
                                           C.POINTER(C.c_double)]
         L.ref_tabu_throughput.restype = C.c_int64
+        L.ref_brute_force.argtypes = [C.c_int, C.c_int, i64p, u64p, C.c_int]
+        L.ref_brute_force.restype = C.c_int
+        L.ref_local_optima.argtypes = [C.c_int, C.c_int]
+        L.ref_local_optima.restype = C.c_int64
+
+    def brute_force(self, n, workers=8, cap=4096):
+        e = C.c_int64(0)
+        w = np.zeros(cap * nwords(n), dtype=np.uint64)
+        c = self.lib.ref_brute_force(n, workers, C.byref(e), _p(w, u64p), cap)
+        if c < 0:
+            raise ValueError("brute force failed")
+        return int(e.value), w[:c * nwords(n)].reshape(c, nwords(n))
+
+    def local_optima(self, n, workers=8):
+        return int(self.lib.ref_local_optima(n, workers))
 
     def rng_draws(self, seed, kinds, lo=None, hi=None):
         k = np.ascontiguousarray(kinds, dtype=np.int32)

@@ -18,6 +18,7 @@
 
 #include "labsolve/correlation_state.hpp"
 #include "labsolve/memetic.hpp"
+#include "labsolve/oracle.hpp"
 #include "labsolve/parallel.hpp"
 #include "labsolve/rng.hpp"
 #include "labsolve/sequence.hpp"
@@ -205,6 +206,32 @@ int ref_run_replicas(int n, int replicas, uint64_t base_seed, int pop,
   if (per_replica)
     for (int i = 0; i < replicas; ++i) fill(report.results[i], &per_replica[i]);
   return 0;
+}
+
+// brute_force_optimum (oracle.cpp:70-110): optimal E and canonical witnesses
+// (words, sorted). Returns the witness count or -1.
+int ref_brute_force(int n, int workers, int64_t* energy, uint64_t* witnesses, int cap) {
+  try {
+    BruteForceResult r = brute_force_optimum(n, workers);
+    *energy = r.optimal_energy;
+    const int nw = (n + 63) / 64;
+    int c = 0;
+    for (const Sequence& s : r.witnesses) {
+      if (c < cap) to_words(s, witnesses + static_cast<size_t>(c) * nw);
+      ++c;
+    }
+    return c;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+int64_t ref_local_optima(int n, int workers) {
+  try {
+    return enumerate_local_optima(n, workers);
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 // CPU baseline: `threads` independent streams running the

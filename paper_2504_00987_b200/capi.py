@@ -45,7 +45,7 @@ EXPORTS = [
     "labs_run_replicas", "labs_solver_create", "labs_solver_destroy", "labs_solver_capacity",
     "labs_solver_run", "labs_solver_request_stop", "labs_solver_status", "labs_solver_counters",
     "labs_solver_results", "labs_solver_export_elites", "labs_solver_import_elites",
-    "labs_bench_int_peak",
+    "labs_bench_int_peak", "labs_exhaustive_optimum", "labs_local_optima",
 ]
 CROSSOVER_UNIFORM = 0
 CROSSOVER_ONE_POINT = 1
@@ -181,6 +181,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.labs_solver_import_elites.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                             C.c_int]
     L.labs_bench_int_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.labs_exhaustive_optimum.argtypes = [C.c_void_p, C.c_int, i64p, u64p, C.c_int64, i64p]
+    L.labs_local_optima.argtypes = [C.c_void_p, C.c_int, i64p]
     _lib = L
     return L
 
@@ -262,6 +264,22 @@ class Context:
 
     def synchronize(self):
         _check(self.L.labs_ctx_synchronize(self.h))
+
+    # -- K5 ---------------------------------------------------------------
+    def exhaustive_optimum(self, n: int, cap: int = 1 << 16):
+        """(optimal E, raw optimal sequences with s_0 = +1) by full enumeration."""
+        e, cnt = C.c_int64(0), C.c_int64(0)
+        w = np.zeros(max(cap, 1), dtype=np.uint64)
+        _check(self.L.labs_exhaustive_optimum(self.h, n, C.byref(e), _ptr(w, u64p), cap,
+                                              C.byref(cnt)))
+        if cnt.value > cap:
+            raise RuntimeError("optimal witness set exceeded the tracking cap")
+        return int(e.value), w[:cnt.value].copy()
+
+    def local_optima(self, n: int) -> int:
+        c = C.c_int64(0)
+        _check(self.L.labs_local_optima(self.h, n, C.byref(c)))
+        return int(c.value)
 
     def int_peak_gops(self) -> float:
         """Measured INT32 lane-instruction rate (roofline denominator)."""

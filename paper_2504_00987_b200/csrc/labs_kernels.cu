@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "labs_b200.h"
+#include "labs_exhaustive.cuh"
 #include "labs_memetic.cuh"
 #include "labs_walker.cuh"
 
@@ -1244,5 +1245,87 @@ extern "C" int labs_bench_int_peak(labs_ctx* ctx, double* gops) {
   LABS_CUDA(cudaGetLastError());
   const double ops = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
   *gops = ops / (best_ms * 1e-3) / 1e9;
+  return LABS_OK;
+}
+
+// ------------------------------------------------- exhaustive oracle (K5) --
+namespace {
+
+template <class F>
+int dispatch_kmax(int n, F&& f) {
+  if (n <= 16) return f(std::integral_constant<int, 16>{});
+  if (n <= 32) return f(std::integral_constant<int, 32>{});
+  if (n <= 48) return f(std::integral_constant<int, 48>{});
+  return f(std::integral_constant<int, 64>{});
+}
+
+int exhaust_launch(labs_ctx* ctx, int n, int mode, unsigned long long* best, const int* target,
+                   uint64_t* out, unsigned long long cap, unsigned long long* cnt) {
+  const int free_bits = n - 1;
+  const int B = free_bits > 18 ? free_bits - 18 : 0;  // >= 2^18 threads when possible
+  const uint64_t blocks = 1ULL << (free_bits - B);
+  const unsigned grid = static_cast<unsigned>((blocks + 127) / 128);
+  return dispatch_kmax(n, [&](auto km) -> int {
+    constexpr int KMAX = decltype(km)::value;
+    k_exhaust<KMAX><<<grid, 128, 0, ctx->stream>>>(n, B, blocks, mode, best, target, out, cap,
+                                                   cnt);
+    LABS_CUDA(cudaGetLastError());
+    return LABS_OK;
+  });
+}
+
+}  // namespace
+
+extern "C" int labs_exhaustive_optimum(labs_ctx* ctx, int n, int64_t* optimal_energy,
+                                       uint64_t* witnesses, int64_t cap, int64_t* count) {
+  if (!ctx || !optimal_energy || !count || cap < 0 || (cap && !witnesses))
+    return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n < 2 || n > 64)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "device exhaustive search needs 2 <= n <= 64");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  DBuf best, tgt, out, cnt;
+  LABS_ALLOC(best, sizeof(unsigned long long));
+  LABS_ALLOC(tgt, sizeof(int));
+  LABS_ALLOC(out, sizeof(uint64_t) * std::max<int64_t>(cap, 1));
+  LABS_ALLOC(cnt, sizeof(unsigned long long));
+  LABS_CUDA(cudaMemsetAsync(best.p, 0xff, sizeof(unsigned long long), ctx->stream));
+  LABS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+  if (int rc = exhaust_launch(ctx, n, 0, best.as<unsigned long long>(), nullptr, nullptr, 0,
+                              nullptr))
+    return rc;
+  unsigned long long e = 0;
+  LABS_D2H(&e, best.p, sizeof(e));
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int ti = static_cast<int>(e);
+  LABS_H2D(tgt.p, &ti, sizeof(int));
+  if (int rc = exhaust_launch(ctx, n, 1, nullptr, tgt.as<int>(), out.as<uint64_t>(),
+                              static_cast<unsigned long long>(cap),
+                              cnt.as<unsigned long long>()))
+    return rc;
+  unsigned long long c = 0;
+  LABS_D2H(&c, cnt.p, sizeof(c));
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (cap && c) LABS_D2H(witnesses, out.p, sizeof(uint64_t) * std::min<uint64_t>(c, cap));
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  *optimal_energy = static_cast<int64_t>(e);
+  *count = static_cast<int64_t>(c);
+  return LABS_OK;
+}
+
+extern "C" int labs_local_optima(labs_ctx* ctx, int n, int64_t* count) {
+  if (!ctx || !count) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n < 2 || n > 64)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "device local-optima census needs 2 <= n <= 64");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  DBuf cnt;
+  LABS_ALLOC(cnt, sizeof(unsigned long long));
+  LABS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+  if (int rc = exhaust_launch(ctx, n, 2, nullptr, nullptr, nullptr, 0,
+                              cnt.as<unsigned long long>()))
+    return rc;
+  unsigned long long c = 0;
+  LABS_D2H(&c, cnt.p, sizeof(c));
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  *count = 2 * static_cast<int64_t>(c);  // the complement half mirrors every optimum
   return LABS_OK;
 }

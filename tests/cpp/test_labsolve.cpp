@@ -12,6 +12,7 @@
 
 #include "labsolve/correlation_state.hpp"
 #include "labsolve/memetic.hpp"
+#include "labsolve/oracle.hpp"
 #include "labsolve/parallel.hpp"
 #include "labsolve/sequence.hpp"
 #include "labsolve/tabu.hpp"
@@ -237,8 +238,23 @@ static void parallel() {
   CHECK_THROWS_AS(run_replicas(broken), std::invalid_argument);
 }
 
+static void oracle() {
+  BruteForceResult r = brute_force_optimum(13, 4);
+  CHECK(r.optimal_energy == 6 && r.witnesses.size() == 1);
+  CHECK(encode_hex(r.witnesses[0]) == "0650");  // README.md:102-104
+  CHECK(enumerate_local_optima(12) == 280);      // README.md:106-107
+  CHECK_THROWS_AS(brute_force_optimum(31), std::invalid_argument);
+  CHECK_THROWS_AS(enumerate_local_optima(25), std::invalid_argument);
+  CHECK(brute_force_optimum_device(32).optimal_energy == 64);
+  // a global optimum is never lost by the tabu walk (test_tabu.cpp:79-85)
+  Rng rng(89);
+  TabuResult res = tabu_search(r.witnesses.front(), TabuParams{}, rng);
+  CHECK(res.energy == 6);
+}
+
 int main() {
   sequences();
+  oracle();
   correlation();
   tabu();
   memetic();

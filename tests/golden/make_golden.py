@@ -174,7 +174,15 @@ def main():
         replicas.append({"n": n, "replicas": R, "base_seed": base, "max_iterations": its,
                          "best": best, "per_replica": per})
 
-    fixtures = {"rng": rng_cases, "kats": kats, "table": table, "targets": targets,
+    # 8. Exhaustive ground truth (oracle.cpp:70-151): optimal E + canonical
+    # witnesses for n = 3..24, strict local-optima census for n = 3..20.
+    exhaustive = []
+    for n in range(3, 25):
+        e, w = ref.brute_force(n)
+        exhaustive.append({"n": n, "E": e, "witnesses": [encode_hex(x, n) for x in w]})
+    local_optima = {n: ref.local_optima(n) for n in range(3, 21)}
+
+    fixtures = {"rng": rng_cases, "exhaustive": exhaustive, "local_optima": local_optima, "kats": kats, "table": table, "targets": targets,
                 "targets_small": small, "probes": probes, "scans": scans, "walks": walks,
                 "memetic": memetic, "replicas": replicas}
     for item in replicas:
@@ -187,7 +195,7 @@ def main():
     with open(path, "w") as f:
         json.dump(fixtures, f, separators=(",", ":"))
     print(f"wrote {path} ({os.path.getsize(path) // 1024} KiB)")
-    _ = double_bits, encode_hex
+    _ = double_bits
 
 
 if __name__ == "__main__":

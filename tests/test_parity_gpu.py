@@ -264,3 +264,37 @@ def test_readme_solve_example(ctx):
     r1 = per[1]
     assert r1["reached_target"] and r1["iterations"] == 98
     assert encode_hex(r1["best"], 20) == "C9EF5"
+
+
+def _canonical_hex(words, n):
+    """canonical() (sequence.cpp:162-169): lexicographic minimum (position 0
+    most significant = hex string order) over the four symmetries."""
+    from paper_2504_00987_b200.sequence import encode_hex, from_spins, spins
+    s = spins(words, n)
+    cands = [s, -s, s[::-1], -s[::-1]]
+    return min(encode_hex(from_spins(c), n) for c in cands)
+
+
+def test_exhaustive_matches_reference(ctx, golden):
+    """brute_force_optimum (oracle.cpp:70-110) for n = 3..24: optimal energy
+    and the canonical witness set, exactly."""
+    for case in golden["exhaustive"]:
+        n = case["n"]
+        e, raw = ctx.exhaustive_optimum(n)
+        assert e == case["E"], n
+        assert sorted({_canonical_hex([w], n) for w in raw}) == case["witnesses"], n
+
+
+def test_exhaustive_proven_optima_and_beyond(ctx, golden):
+    """targets_small.txt (proven optima, n = 2..30) and the literature optimum
+    E(32) = 64 (Packebusch & Mertens 2016), beyond the reference's n <= 30."""
+    for n_str, e_want in golden["targets_small"].items():
+        e, _ = ctx.exhaustive_optimum(int(n_str), cap=4096)
+        assert e == e_want, n_str
+    e, _ = ctx.exhaustive_optimum(32, cap=4096)
+    assert e == 64
+
+
+def test_local_optima_census_matches_reference(ctx, golden):
+    for n_str, want in golden["local_optima"].items():
+        assert ctx.local_optima(int(n_str)) == want, n_str
