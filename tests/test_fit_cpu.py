@@ -22,3 +22,25 @@ def test_student_t_against_scipy():
     for dof, want in [(1, 12.706204736174707), (2, 4.302652729749464),
                       (10, 2.228138851986274), (30, 2.042272456301238)]:
         assert abs(st.t.ppf(0.975, dof) - want) < 1e-9
+
+
+def test_python_fit_matches_reference_semantics():
+    """paper_2504_00987_b200.tts mirrors fit.cpp: quantiles, censoring, fit."""
+    import math
+    import scipy.stats as st
+    from paper_2504_00987_b200 import tts
+    assert tts.quantile([1.0, 2.0, 3.0, 4.0], 0.25) == 1.75
+    s = [{"n": 10, "runtime": 1.0, "reachedTarget": True},
+         {"n": 10, "runtime": 3.0, "reachedTarget": True},
+         {"n": 10, "runtime": 99.0, "reachedTarget": False},
+         {"n": 12, "runtime": 50.0, "reachedTarget": False}]
+    assert tts.median_runtime_by_n(s) == {10: 2.0}
+    ex = [{"n": n, "runtime": 2e-7 * 1.3 ** n, "reachedTarget": True} for n in range(20, 41)]
+    f = tts.fit_exponential(ex, 20, 40)
+    assert abs(f["b"] - 1.3) < 1e-12 and abs(f["a"] / 2e-7 - 1) < 1e-9
+    for dof in (1, 3, 7, 19, 50):
+        assert abs(tts.student_t_quantile(dof, 0.975) - st.t.ppf(0.975, dof)) < 1e-8
+    noisy = [{"n": n, "runtime": 1e-6 * 1.25 ** n * math.exp(0.3 * math.sin(n)),
+              "reachedTarget": True} for n in range(10, 31)]
+    f = tts.fit_exponential(noisy, 10, 30)
+    assert f["b_ci"][0] < 1.25 < f["b_ci"][1]
