@@ -182,24 +182,11 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
     epoch_s = args.epoch_ms / 1e3
 
-    # islands: k elites per GPU, gathered over NCCL between steps
-    k_el = 16
-    nw = (n + 63) // 64
-    el_w = torch.zeros(k_el * nw, dtype=torch.int64, device=f"cuda:{local}")
-    el_e = torch.zeros(k_el, dtype=torch.int64, device=f"cuda:{local}")
-    all_w = torch.zeros(world * k_el * nw, dtype=torch.int64, device=f"cuda:{local}")
-    all_e = torch.zeros(world * k_el, dtype=torch.int64, device=f"cuda:{local}")
-
-    def exchange(step):
-        solver.export_elites(k_el, el_w.data_ptr(), el_e.data_ptr())
-        with torch.cuda.stream(ext):
-            if world > 1:
-                dist.all_gather_into_tensor(all_w, el_w)
-                dist.all_gather_into_tensor(all_e, el_e)
-            else:
-                all_w.copy_(el_w)
-                all_e.copy_(el_e)
-        solver.import_elites(world * k_el, all_w.data_ptr(), all_e.data_ptr(), rotation=step)
+    # islands: k elites per GPU, all_gathered over NCCL between steps
+    isl = None
+    if args.islands:
+        from paper_2504_00987_b200.islands import Islands
+        isl = Islands(solver, n, k_elites=16, device=torch.device("cuda", local))
 
     for _ in range(args.warmup):
         solver.run(epoch_seconds=epoch_s, race=False)
@@ -222,8 +209,8 @@ def main():
             launches += 1
             with torch.cuda.stream(ext):
                 ends[k].record(ext)
-            if args.islands and (k + 1) % args.islands == 0:
-                exchange(k)
+            if isl is not None and (k + 1) % args.islands == 0:
+                isl.exchange(rotation=k)
         ctx.synchronize()
         torch.cuda.synchronize()
     if world > 1:

@@ -47,6 +47,15 @@
 
 namespace labsk {
 
+// redux.sync.min over the full warp. The walker's control flow is warp-
+// uniform by construction, so the intrinsic's divergence guard is dead
+// weight on the hot path.
+__device__ __forceinline__ int warp_min(int v) {
+  int r;
+  asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t lowmask(int x);
 
 template <int NS>
@@ -336,9 +345,9 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
     kmin_hi = min(kmin_hi, adm[b] ? dE[b] * 256 + (255 - 32 * b - ln) : INT_MAX);
 #endif
   }
-  kmin = __reduce_min_sync(kFull, kmin);
+  kmin = warp_min(kmin);
 #if LABS_TIE_DUAL
-  if (!FULL_TIES && tie_rule == 0) kmin_hi = __reduce_min_sync(kFull, kmin_hi);
+  if (!FULL_TIES && tie_rule == 0) kmin_hi = warp_min(kmin_hi);
 #endif
   if (kmin == INT_MAX) {
     pos = static_cast<int>(uniform_int(rng, 0, n - 1));
@@ -361,7 +370,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
     int k2 = INT_MAX;
 #pragma unroll
     for (int b = 0; b < NS; ++b) k2 = min(k2, key[b] == kmin ? INT_MAX : key[b]);
-    k2 = __reduce_min_sync(kFull, k2);
+    k2 = warp_min(k2);
     tied = (k2 >> 8) == dmin;
 #endif
   }
@@ -386,7 +395,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
 // tabu_search (proj/src/tabu.cpp:17-56) for one walker. `in` is the start
 // sequence; on return `best` holds the best visited sequence (the start
 // counts as visited) and the return value is its energy.
-template <int NS, bool ASP, class R>
+template <int NS, bool ASP, bool TRACE, class R>
 __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
                                          const uint32_t (&in)[NS], R& rng,
                                          const TabuCfg& cfg,
@@ -432,7 +441,7 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
       bestE = w.E;
       w.chunks(best);
     }
-    if (trace && lane_id() == 0) {
+    if (TRACE && lane_id() == 0) {
       StepRec rec;
       rec.iteration = t;
       rec.position = pos;
@@ -450,9 +459,14 @@ template <int NS, class R>
 __device__ __forceinline__ int tabu_walk(Walker<NS>& w, int n, const uint32_t (&in)[NS],
                                          R& rng, const TabuCfg& cfg, uint32_t (&best)[NS],
                                          int* info, StepRec* trace, int* steps_out) {
+  if (trace) {
+    if (cfg.aspiration)
+      return tabu_walk_impl<NS, true, true>(w, n, in, rng, cfg, best, info, trace, steps_out);
+    return tabu_walk_impl<NS, false, true>(w, n, in, rng, cfg, best, info, trace, steps_out);
+  }
   if (cfg.aspiration)
-    return tabu_walk_impl<NS, true>(w, n, in, rng, cfg, best, info, trace, steps_out);
-  return tabu_walk_impl<NS, false>(w, n, in, rng, cfg, best, info, trace, steps_out);
+    return tabu_walk_impl<NS, true, false>(w, n, in, rng, cfg, best, info, nullptr, steps_out);
+  return tabu_walk_impl<NS, false, false>(w, n, in, rng, cfg, best, info, nullptr, steps_out);
 }
 
 // u64 words (global layout) <-> 32-bit chunks (register layout).
