@@ -235,6 +235,27 @@ __device__ __forceinline__ long long uniform_int(R& rng, long long lo,
   return static_cast<long long>(static_cast<uint64_t>(lo) + __umul64hi(x, range));
 }
 
+// uniform_int(0, r - 1) for a known 32-bit range r >= 1: the same Lemire
+// arithmetic (and draw count) as uniform_int, without the range dispatch.
+template <class R>
+__device__ __forceinline__ int uniform_below(R& rng, uint32_t r32) {
+  uint64_t x = rng.next();
+  uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+  uint64_t p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+  if (static_cast<uint32_t>(p1) == 0 && static_cast<uint32_t>(p0) < r32) {
+    const uint64_t range = r32;
+    const uint64_t thr = (0ULL - range) % range;
+    uint64_t low = (p1 << 32) | static_cast<uint32_t>(p0);
+    while (low < thr) {
+      x = rng.next();
+      p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+      p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+      low = (p1 << 32) | static_cast<uint32_t>(p0);
+    }
+  }
+  return static_cast<int>(p1 >> 32);
+}
+
 template <class R>
 __device__ __forceinline__ double uniform01(R& rng) {
   return u01_from_bits(rng.next());

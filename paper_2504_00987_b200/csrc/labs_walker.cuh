@@ -230,8 +230,10 @@ struct Walker {
 
   // Spin store of the previous flip, performed by every lane before it reads
   // S (each lane then observes its own store).
+  // (pend_pos = -1, pend_val = 0 after init rewrites the zero padding byte
+  // S[L-1], so the store needs no guard.)
   __device__ __forceinline__ void flush_spin() {
-    if (pend_pos >= 0) sm->S[L + pend_pos] = static_cast<int8_t>(pend_val);
+    sm->S[L + pend_pos] = static_cast<int8_t>(pend_val);
   }
 
   // Commit flip `pos` (warp-uniform); its expiry becomes t + tenure. Reads
@@ -350,7 +352,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
   if (!FULL_TIES && tie_rule == 0) kmin_hi = warp_min(kmin_hi);
 #endif
   if (kmin == INT_MAX) {
-    pos = static_cast<int>(uniform_int(rng, 0, n - 1));
+    pos = uniform_below(rng, static_cast<uint32_t>(n));
     dEp = at_position<NS>(dE, pos);
     fallback = 1;
     ntie = 0;
@@ -386,7 +388,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
     }
     ntie = cnt;
     if (cnt > 1 && tie_rule == 0) {
-      const int r = static_cast<int>(uniform_int(rng, 0, static_cast<long long>(cnt) - 1));
+      const int r = uniform_below(rng, static_cast<uint32_t>(cnt));
       if (r) pos = nth_hit<NS>(hit, msk, r);
     }
   }
@@ -416,6 +418,7 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
   w.init(n, in);
   int bestE = w.E;
   const int tie_rule = cfg.tie_rule;
+  const uint32_t tenure_range = static_cast<uint32_t>(max_t - min_t + 1);
 #pragma unroll
   for (int b = 0; b < NS; ++b) best[b] = in[b] & lowmask(n - 32 * b);
   for (int t = 1; t <= m; ++t) {
@@ -435,7 +438,7 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
     int pos, dEp, fb, ntie;
     uint32_t msk[NS];
     select_move<NS, false>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
-    const int tenure = static_cast<int>(uniform_int(rng, min_t, max_t));
+    const int tenure = min_t + uniform_below(rng, tenure_range);
     w.apply(pos, dEp, t, tenure);
     if (w.E < bestE) {
       bestE = w.E;
