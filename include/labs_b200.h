@@ -265,6 +265,10 @@ int labs_solver_export_elites(labs_solver* s, int k, uint64_t* d_words,
 int labs_solver_import_elites(labs_solver* s, int count,
                               const uint64_t* d_words,
                               const int64_t* d_energies, int rotation);
+/* Copy every population out (host buffers, synchronizing): words
+ * replicas x K x ceil(n/64), energies replicas x K. For inspection and
+ * checkpointing between epochs. */
+int labs_solver_population(labs_solver* s, uint64_t* words, int32_t* energies);
 
 /* ------------------------------------- K5: exhaustive ground truth ------ */
 /* Replaces brute_force_optimum / enumerate_local_optima

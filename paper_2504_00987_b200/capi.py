@@ -46,6 +46,7 @@ EXPORTS = [
     "labs_solver_run", "labs_solver_request_stop", "labs_solver_status", "labs_solver_counters",
     "labs_solver_results", "labs_solver_export_elites", "labs_solver_import_elites",
     "labs_bench_int_peak", "labs_exhaustive_optimum", "labs_local_optima",
+    "labs_solver_population",
 ]
 CROSSOVER_UNIFORM = 0
 CROSSOVER_ONE_POINT = 1
@@ -183,6 +184,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.labs_bench_int_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     L.labs_exhaustive_optimum.argtypes = [C.c_void_p, C.c_int, i64p, u64p, C.c_int64, i64p]
     L.labs_local_optima.argtypes = [C.c_void_p, C.c_int, i64p]
+    L.labs_solver_population.argtypes = [C.c_void_p, u64p, i32p]
     _lib = L
     return L
 
@@ -479,6 +481,14 @@ class Solver:
                                int(tr[i * self.trace_cap + j].child_energy))
                               for j in range(int(tl[i]))]
         return reps
+
+    def population(self):
+        """(words[R, K, W], energies[R, K]) copied out of HBM."""
+        K = self.params.population_size
+        w = np.zeros((self.replicas, K, nwords(self.n)), dtype=np.uint64)
+        e = np.zeros((self.replicas, K), dtype=np.int32)
+        _check(self.L.labs_solver_population(self.h, _ptr(w, u64p), _ptr(e, i32p)))
+        return w, e
 
     def export_elites(self, k: int, d_words: int, d_energies: int):
         _check(self.L.labs_solver_export_elites(self.h, k, C.c_void_p(d_words),

@@ -1160,6 +1160,17 @@ int labs_solver_import_elites(labs_solver* s, int count, const uint64_t* d_words
   return LABS_OK;
 }
 
+int labs_solver_population(labs_solver* s, uint64_t* words, int32_t* energies) {
+  if (!s || !words || !energies) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  const size_t R = s->R, K = s->K, nw = s->nw;
+  LABS_D2H(words, s->pop.p, sizeof(uint64_t) * R * K * nw);
+  LABS_D2H(energies, s->popE.p, sizeof(int32_t) * R * K);
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LABS_OK;
+}
+
 int labs_memetic(labs_ctx* ctx, int n, const labs_memetic_params* params, uint64_t seed,
                  const volatile int32_t* stop, int replica_id, labs_run_result* out,
                  labs_memetic_record* trace, int64_t trace_cap, int64_t* trace_len) {

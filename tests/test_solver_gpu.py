@@ -1,0 +1,118 @@
+"""Device solver API (labs_solver_*): epoch invariance, production policies,
+island export/import semantics. Complements the reference-parity tests."""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Oracle
+from paper_2504_00987_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+
+def _results(sv):
+    return [(r["best"].tolist(), r["best_energy"], r["iterations"]) for r in sv.results()]
+
+
+def test_epochs_do_not_change_trajectories(ctx):
+    """Cutting a run into epochs (the island model's exchange points) leaves
+    every replica's trajectory bit-identical to one uninterrupted run."""
+    n, R, iters = 48, 64, 12
+    p = capi.memetic_params(target_energy=0, max_iterations=iters)
+    one = capi.Solver(ctx, n, R, base_seed=5, params=p)
+    one.run(race=False)
+    cut = capi.Solver(ctx, n, R, base_seed=5, params=p)
+    for _ in range(iters):
+        cut.run(epoch_iterations=1, race=False)
+    assert cut.status()["running"] == 0
+    assert _results(one) == _results(cut)
+    w1, e1 = one.population()
+    w2, e2 = cut.population()
+    assert (w1 == w2).all() and (e1 == e2).all()
+
+
+def test_solver_matches_run_replicas_and_oracle(ctx):
+    n, R, iters = 30, 5, 6
+    p = capi.memetic_params(target_energy=0, max_iterations=iters)
+    sv = capi.Solver(ctx, n, R, base_seed=100, params=p, replica_offset=3)
+    sv.run(race=False)
+    o = Oracle()
+    for r in sv.results():
+        # global id = offset + r, seed = base + id (parallel.cpp:38)
+        want = o.memetic(n, 100 + r["replica_id"], max_iterations=iters)
+        assert r["seed"] == 100 + r["replica_id"]
+        assert r["best_energy"] == want["best_energy"] and r["best"].tolist() == want["best"]
+
+
+def test_population_energies_are_consistent(ctx, oracle):
+    n, R = 40, 8
+    sv = capi.Solver(ctx, n, R, base_seed=1, params=capi.memetic_params(max_iterations=5))
+    sv.run(race=False)
+    w, e = sv.population()
+    for r in range(R):
+        for k in range(0, 100, 17):
+            assert oracle.energy(n, w[r, k]) == e[r, k]
+
+
+@pytest.mark.parametrize("kind", [capi.RNG_PHILOX, capi.RNG_MT19937_64])
+@pytest.mark.parametrize("cross,repl", [(capi.CROSSOVER_ONE_POINT, capi.REPLACE_WORST),
+                                        (capi.CROSSOVER_UNIFORM, capi.REPLACE_WORST),
+                                        (capi.CROSSOVER_ONE_POINT, capi.REPLACE_RANDOM)])
+def test_production_policies(ctx, oracle, kind, cross, repl):
+    """One-point crossover, elite replacement, Philox: reproducible per seed,
+    energies consistent, elite replacement never raises the population max."""
+    n, R = 36, 16
+    p = capi.memetic_params(target_energy=0, max_iterations=6, rng_kind=kind, crossover=cross,
+                            replacement=repl, tie_rule=capi.TIE_LOWEST)
+    a = capi.Solver(ctx, n, R, base_seed=9, params=p)
+    a.run(epoch_iterations=1, race=False)
+    w0, e0 = a.population()
+    a.run(race=False)
+    b = capi.Solver(ctx, n, R, base_seed=9, params=p)
+    b.run(race=False)
+    assert _results(a) == _results(b)
+    w, e = a.population()
+    for r in range(0, R, 5):
+        for k in range(0, 100, 23):
+            assert oracle.energy(n, w[r, k]) == e[r, k]
+    if repl == capi.REPLACE_WORST:
+        assert (e.max(axis=1) <= e0.max(axis=1)).all()
+    for r in a.results():
+        assert oracle.energy(n, r["best"]) == r["best_energy"]
+
+
+def test_island_export_import(ctx):
+    import torch
+    n, R, k = 40, 32, 4
+    sv = capi.Solver(ctx, n, R, base_seed=11, params=capi.memetic_params(max_iterations=3))
+    sv.run(epoch_iterations=2, race=False)
+    nw = 1
+    d_w = torch.zeros(k * nw, dtype=torch.int64, device="cuda")
+    d_e = torch.zeros(k, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    sv.export_elites(k, d_w.data_ptr(), d_e.data_ptr())
+    sv.sync()
+    res = sv.results()
+    bestE = sorted(r["best_energy"] for r in res)
+    got = d_e.cpu().tolist()
+    assert got == bestE[:k]
+    words = d_w.cpu().numpy().view(np.uint64)
+    byE = {}
+    for r in res:
+        byE.setdefault(r["best_energy"], []).append(r["best"][0])
+    for i in range(k):
+        assert words[i] in byE[got[i]]
+    # import an elite better than every member: each replica's worst slot takes it
+    _, e_before = sv.population()
+    elite_e = int(e_before.min()) - 1  # synthetic key, strictly better than all
+    d_w2 = torch.tensor([int(words[0].astype(np.int64))], dtype=torch.int64, device="cuda")
+    d_e2 = torch.tensor([elite_e], dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    sv.import_elites(1, d_w2.data_ptr(), d_e2.data_ptr(), rotation=0)
+    sv.sync()
+    w_after, e_after = sv.population()
+    for r in range(R):
+        if res[r]["iterations"] >= 3:
+            continue  # finished replicas do not import
+        worst = int(np.argmax(e_before[r]))
+        assert e_after[r, worst] == elite_e
+        assert w_after[r, worst, 0] == words[0]
