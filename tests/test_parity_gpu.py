@@ -298,3 +298,23 @@ def test_exhaustive_proven_optima_and_beyond(ctx, golden):
 def test_local_optima_census_matches_reference(ctx, golden):
     for n_str, want in golden["local_optima"].items():
         assert ctx.local_optima(int(n_str)) == want, n_str
+
+
+def test_solve_cli_wire_format(tmp_path):
+    """README.md:110-117: `labs solve --n 20 --target 26 --replicas 2 --seed 42`."""
+    import json
+    import subprocess
+    import sys
+    out = tmp_path / "solve.jsonl"
+    r = subprocess.run([sys.executable, "-m", "paper_2504_00987_b200.solve", "--n", "20",
+                        "--target", "26", "--replicas", "2", "--seed", "42", "--time-limit",
+                        "30", "--out", str(out)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout)
+    assert list(d) == sorted(d)
+    assert d["bestE"] == 26 and d["reachedTarget"] and d["n"] == 20
+    assert d["seed"] == 42 + d["replicaId"]
+    assert json.loads(out.read_text().splitlines()[0]) == d
+    bad = subprocess.run([sys.executable, "-m", "paper_2504_00987_b200.solve", "--n", "1"],
+                         capture_output=True, text=True, timeout=120)
+    assert bad.returncode == 2
