@@ -155,10 +155,13 @@ def run_tts(ctx, n_values, targets, reps=5, replicas=0, base_seed=7, time_limit=
             sv.run(race=True)
             st = sv.status()
             dt = time.perf_counter() - t0
+            from paper_2504_00987_b200.sequence import encode_hex
+            win = sv.results()[st["best_replica"]]
             sv.close()
             rec = {"n": n, "targetE": targets[n], "runtime": dt,
                    "reachedTarget": st["best_energy"] <= targets[n], "seed": seed,
-                   "replicas": R, "bestE": st["best_energy"]}
+                   "replicas": R, "bestE": st["best_energy"],
+                   "bestSeq": encode_hex(win["best"], n), "bestReplica": st["best_replica"]}
             out.append(rec)
             if log:
                 log(rec)
