@@ -29,7 +29,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -37,7 +36,6 @@ import sys
 import threading
 import time
 
-import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -245,7 +243,7 @@ def main():
             traffic = None
 
     # e2e through the reference-facing C-ABI call with host buffers
-    e2e_iters = 400
+    e2e_iters = 2000
     e2e_params = capi.memetic_params(target_energy=0, max_iterations=e2e_iters,
                                      rng_kind=rng_kind)
     ctx.run_replicas(n, R, 7, e2e_params)  # warm

@@ -17,7 +17,6 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-from dataclasses import dataclass, field
 
 import numpy as np
 
