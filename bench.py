@@ -233,12 +233,14 @@ def main():
     achieved_gops = per_gpu * OPS_PER_FLIP_EVAL / 1e9
     # DRAM bytes per launch from the committed ncu capture, scaled to this
     # run's epoch length (the kernel's traffic is per memetic iteration).
-    traffic = None
+    traffic, issue = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            per_ms = json.load(open(prof)).get(f"k_memetic_n{n}_dram_bytes_per_ms")
+            pj = json.load(open(prof))
+            per_ms = pj.get(f"k_memetic_n{n}_dram_bytes_per_ms")
             traffic = per_ms * (time_ms / args.steps) if per_ms else None
+            issue = pj.get(f"k_memetic_n{n}_issue_slots_busy")
         except Exception:
             traffic = None
 
@@ -281,7 +283,8 @@ def main():
                      "unit": "Gop/s", "frac": achieved_gops / peak_gops, "traffic": traffic,
                      "ops_per_flip_eval": OPS_PER_FLIP_EVAL,
                      "peak_source": "measured on this device (labs_bench_int_peak)",
-                     "lag_term_equiv_frac": per_gpu * (n - 1) / (peak_gops * 1e9)},
+                     "lag_term_equiv_frac": per_gpu * (n - 1) / (peak_gops * 1e9),
+                     "issue_slots_busy_ncu": issue},
         "e2e": {"value": e2e_value, "unit": "flip-evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "call": f"labs_run_replicas(n={n}, replicas={R}, max_iterations={e2e_iters})"},

@@ -43,7 +43,7 @@ __host__ __device__ constexpr int min_blocks() {
 template <int NS, bool MT>
 struct WarpSlot {
   uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
-  uint64_t out[MT ? kMtN : 1];   // tempered outputs of the current block
+  uint64_t out[MT ? kMtN : PhiloxRng::kBlock];  // tempered block / Philox block
   WalkSmem<NS> walk;
 };
 
@@ -246,8 +246,7 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_tabu(WalkArgs
       rng.k1 = static_cast<uint32_t>(A.seed >> 32);
       rng.s0 = static_cast<uint32_t>(item);
       rng.s1 = 0x4C414253u;  // "LABS"
-      rng.ctr = A.ctr_base;
-      rng.cache = (rng.ctr & 1ULL) ? rng.block_half(rng.ctr) : 0ULL;
+      rng.bind(sl.out, A.ctr_base);
       for (int k = 0; k < A.walks; ++k) {
         int steps = 0;
         bestE = tabu_walk<NS>(w, n, cur, rng, A.cfg, best,
@@ -300,8 +299,7 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_memetic(Memet
       rng.k1 = static_cast<uint32_t>(A.base_seed >> 32);
       rng.s0 = static_cast<uint32_t>(A.replica_offset + r);
       rng.s1 = 0x4D454D45u;  // "MEME"
-      rng.ctr = A.ctr[r];
-      rng.cache = (rng.ctr & 1ULL) ? rng.block_half(rng.ctr) : 0ULL;
+      rng.bind(sl.out, A.ctr[r]);
       memetic_replica<NS>(A, r, w, rng);
       if (lane_id() == 0) A.ctr[r] = rng.ctr;
     }

@@ -159,40 +159,52 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0,
   }
 }
 
+// Draws are served from a per-warp block of 64 in shared memory: a refill
+// has lane l compute Philox block (base/2 + l), i.e. draws base + 2l and
+// base + 2l + 1, so the 10-round cost is paid once per 64 draws and spread
+// over the warp. The stream is defined per draw index d (block d >> 1, half
+// d & 1), independent of the buffering.
+__device__ __noinline__ void philox_refill(uint32_t buf, uint64_t base, uint32_t k0,
+                                           uint32_t k1, uint32_t s0, uint32_t s1) {
+  const uint64_t blk = (base >> 1) + static_cast<uint64_t>(lane_id());
+  uint32_t c[4] = {static_cast<uint32_t>(blk), static_cast<uint32_t>(blk >> 32), s0, s1};
+  philox4x32_10(c, k0, k1);
+  sts_u64(buf + 16u * lane_id(), static_cast<uint64_t>(c[1]) << 32 | c[0]);
+  sts_u64(buf + 16u * lane_id() + 8u, static_cast<uint64_t>(c[3]) << 32 | c[2]);
+  __syncwarp();
+}
+
 struct PhiloxRng {
+  static constexpr int kBlock = 64;
   uint32_t k0, k1;   // key = seed
   uint32_t s0, s1;   // stream (walker / replica id)
   uint64_t ctr;      // next draw index
-  uint64_t cache;    // upper half of block ctr>>1 when ctr is odd
+  uint32_t buf_s;    // shared-window address of the current 64-draw block
 
-  __device__ __forceinline__ uint64_t block_half(uint64_t d) const {
-    uint32_t c[4] = {static_cast<uint32_t>(d >> 1),
-                     static_cast<uint32_t>(d >> 33), s0, s1};
-    philox4x32_10(c, k0, k1);
-    return (d & 1ULL) ? (static_cast<uint64_t>(c[3]) << 32 | c[2])
-                      : (static_cast<uint64_t>(c[1]) << 32 | c[0]);
+  // Bind to a shared buffer of kBlock words and fill the block holding ctr.
+  __device__ __forceinline__ void bind(uint64_t* buf, uint64_t c) {
+    buf_s = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+    ctr = c;
+    philox_refill(buf_s, ctr & ~static_cast<uint64_t>(kBlock - 1), k0, k1, s0, s1);
   }
   __device__ __forceinline__ uint64_t next() {
-    uint64_t v;
-    if (ctr & 1ULL) {
-      v = cache;
-    } else {
-      uint32_t c[4] = {static_cast<uint32_t>(ctr >> 1),
-                       static_cast<uint32_t>(ctr >> 33), s0, s1};
-      philox4x32_10(c, k0, k1);
-      v = static_cast<uint64_t>(c[1]) << 32 | c[0];
-      cache = static_cast<uint64_t>(c[3]) << 32 | c[2];
-    }
+    const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
+    if (off == 0) philox_refill(buf_s, ctr, k0, k1, s0, s1);
+    const uint64_t v = lds_u64(buf_s + 8u * off);
     ++ctr;
     return v;
   }
-  __device__ __forceinline__ int room() { return 1 << 30; }
+  __device__ __forceinline__ int room() {
+    const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
+    if (off == 0) philox_refill(buf_s, ctr, k0, k1, s0, s1);
+    return kBlock - static_cast<int>(off);
+  }
   __device__ __forceinline__ uint64_t peek_lane(int i) const {
-    return block_half(ctr + static_cast<uint64_t>(i));
+    return lds_u64(buf_s + 8u * ((static_cast<uint32_t>(ctr) & (kBlock - 1)) + i));
   }
   __device__ __forceinline__ void advance(int count) {
-    uint64_t nc = ctr + static_cast<uint64_t>(count);
-    if (nc & 1ULL) cache = block_half(nc);  // keep the odd-index cache valid
+    const uint64_t nc = ctr + static_cast<uint64_t>(count);
+    // crossing into a new block mid-way is impossible: count <= room()
     ctr = nc;
   }
 };
