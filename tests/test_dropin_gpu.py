@@ -17,3 +17,11 @@ def test_cpp_dropin_suite():
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_plain_c_client():
+    exe = os.path.join(ROOT, "tests", "cpp", "test_capi")
+    assert os.path.exists(exe), "build with __graft_entry__.build()"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
