@@ -269,6 +269,15 @@ int labs_solver_import_elites(labs_solver* s, int count,
  * replicas x K x ceil(n/64), energies replicas x K. For inspection and
  * checkpointing between epochs. */
 int labs_solver_population(labs_solver* s, uint64_t* words, int32_t* energies);
+/* Checkpoint / resume for long runs: the complete replica state (populations,
+ * energies, bests, counters, RNG states, traces) as one host blob.
+ * state_size returns the byte count; load requires a solver created with the
+ * same n, replicas, params and trace_cap (checked; LABS_ERR_INVALID_ARGUMENT
+ * otherwise). A resumed run continues every replica's trajectory exactly;
+ * max_seconds budgets restart from the load time. */
+int64_t labs_solver_state_size(labs_solver* s);
+int labs_solver_save(labs_solver* s, void* blob);
+int labs_solver_load(labs_solver* s, const void* blob);
 
 /* ------------------------------------- K5: exhaustive ground truth ------ */
 /* Replaces brute_force_optimum / enumerate_local_optima

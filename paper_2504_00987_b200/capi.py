@@ -45,7 +45,7 @@ EXPORTS = [
     "labs_solver_run", "labs_solver_request_stop", "labs_solver_status", "labs_solver_counters",
     "labs_solver_results", "labs_solver_export_elites", "labs_solver_import_elites",
     "labs_bench_int_peak", "labs_exhaustive_optimum", "labs_local_optima",
-    "labs_solver_population",
+    "labs_solver_population", "labs_solver_state_size", "labs_solver_save", "labs_solver_load",
 ]
 CROSSOVER_UNIFORM = 0
 CROSSOVER_ONE_POINT = 1
@@ -184,6 +184,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.labs_exhaustive_optimum.argtypes = [C.c_void_p, C.c_int, i64p, u64p, C.c_int64, i64p]
     L.labs_local_optima.argtypes = [C.c_void_p, C.c_int, i64p]
     L.labs_solver_population.argtypes = [C.c_void_p, u64p, i32p]
+    L.labs_solver_state_size.argtypes = [C.c_void_p]
+    L.labs_solver_state_size.restype = C.c_int64
+    L.labs_solver_save.argtypes = [C.c_void_p, C.c_void_p]
+    L.labs_solver_load.argtypes = [C.c_void_p, C.c_void_p]
     _lib = L
     return L
 
@@ -488,6 +492,18 @@ class Solver:
         e = np.zeros((self.replicas, K), dtype=np.int32)
         _check(self.L.labs_solver_population(self.h, _ptr(w, u64p), _ptr(e, i32p)))
         return w, e
+
+    def save(self) -> bytes:
+        """Checkpoint of every replica's complete state (labs_solver_save)."""
+        size = int(self.L.labs_solver_state_size(self.h))
+        buf = (C.c_ubyte * size)()
+        _check(self.L.labs_solver_save(self.h, buf))
+        return bytes(buf)
+
+    def load(self, blob: bytes):
+        """Resume from a checkpoint made by a solver with the same setup."""
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(self.L.labs_solver_load(self.h, buf))
 
     def export_elites(self, k: int, d_words: int, d_energies: int):
         _check(self.L.labs_solver_export_elites(self.h, k, C.c_void_p(d_words),

@@ -1169,6 +1169,104 @@ int labs_solver_population(labs_solver* s, uint64_t* words, int32_t* energies) {
   return LABS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+struct BlobHeader {
+  uint64_t magic;  // "LABSCKP1"
+  int32_t n, R, K, nw, rng_kind, crossover, replacement, pad_;
+  int64_t trace_cap;
+};
+constexpr uint64_t kBlobMagic = 0x31504B4353424C4CULL;
+
+// (device buffer, bytes) in blob order.
+std::vector<std::pair<void*, size_t>> state_parts(labs_solver* s) {
+  const size_t R = s->R, K = s->K, nw = s->nw;
+  std::vector<std::pair<void*, size_t>> v = {
+      {s->pop.p, sizeof(uint64_t) * R * K * nw}, {s->popE.p, sizeof(int32_t) * R * K},
+      {s->best.p, sizeof(uint64_t) * R * nw},    {s->bestE.p, sizeof(int32_t) * R},
+      {s->iters.p, sizeof(int64_t) * R},         {s->status.p, sizeof(int32_t) * R},
+      {s->init.p, sizeof(int32_t) * R},          {s->tend.p, sizeof(int64_t) * R},
+      {s->order.p, sizeof(int32_t) * R},         {s->counter.p, sizeof(int32_t)},
+      {s->stop.p, sizeof(int32_t)},              {s->tabu_total.p, sizeof(unsigned long long)},
+      {s->tabu_rep.p, sizeof(int64_t) * R}};
+  if (s->mt) v.push_back({s->rng.p, sizeof(labs_rng_state) * R});
+  else v.push_back({s->ctr.p, sizeof(uint64_t) * R});
+  if (s->trace_cap) {
+    v.push_back({s->trace.p, sizeof(int64_t) * 3 * R * s->trace_cap});
+    v.push_back({s->trace_len.p, sizeof(int64_t) * R});
+  }
+  return v;
+}
+
+BlobHeader header_of(labs_solver* s) {
+  BlobHeader h{};
+  h.magic = kBlobMagic;
+  h.n = s->n;
+  h.R = s->R;
+  h.K = s->K;
+  h.nw = s->nw;
+  h.rng_kind = s->p.rng_kind;
+  h.crossover = s->p.crossover;
+  h.replacement = s->p.replacement;
+  h.trace_cap = s->trace_cap;
+  return h;
+}
+
+__global__ void k_restamp(int R, int64_t* t0) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) t0[r] = globaltimer_ns();
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t labs_solver_state_size(labs_solver* s) {
+  if (!s) return -1;
+  int64_t total = sizeof(BlobHeader);
+  for (auto& part : state_parts(s)) total += static_cast<int64_t>(part.second);
+  return total;
+}
+
+int labs_solver_save(labs_solver* s, void* blob) {
+  if (!s || !blob) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  unsigned char* out = static_cast<unsigned char*>(blob);
+  const BlobHeader h = header_of(s);
+  std::memcpy(out, &h, sizeof h);
+  size_t off = sizeof h;
+  for (auto& part : state_parts(s)) {
+    LABS_D2H(out + off, part.first, part.second);
+    off += part.second;
+  }
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LABS_OK;
+}
+
+int labs_solver_load(labs_solver* s, const void* blob) {
+  if (!s || !blob) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  const unsigned char* in = static_cast<const unsigned char*>(blob);
+  BlobHeader h;
+  std::memcpy(&h, in, sizeof h);
+  const BlobHeader want = header_of(s);
+  if (std::memcmp(&h, &want, sizeof h) != 0)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "checkpoint does not match this solver");
+  size_t off = sizeof h;
+  for (auto& part : state_parts(s)) {
+    LABS_H2D(part.first, in + off, part.second);
+    off += part.second;
+  }
+  k_restamp<<<(s->R + 127) / 128, 128, 0, ctx->stream>>>(s->R, s->t0.as<int64_t>());
+  LABS_CUDA(cudaGetLastError());
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LABS_OK;
+}
+
 int labs_memetic(labs_ctx* ctx, int n, const labs_memetic_params* params, uint64_t seed,
                  const volatile int32_t* stop, int replica_id, labs_run_result* out,
                  labs_memetic_record* trace, int64_t trace_cap, int64_t* trace_len) {
