@@ -116,3 +116,26 @@ def test_island_export_import(ctx):
         worst = int(np.argmax(e_before[r]))
         assert e_after[r, worst] == elite_e
         assert w_after[r, worst, 0] == words[0]
+
+
+def test_checkpoint_resume_is_exact(ctx):
+    """Save after some epochs, resume in a fresh solver: the continued run is
+    bit-identical to an uninterrupted one (SURVEY §5 checkpoint/resume)."""
+    n, R = 52, 40
+    for kind in (capi.RNG_MT19937_64, capi.RNG_PHILOX):
+        p = capi.memetic_params(target_energy=0, max_iterations=10, rng_kind=kind)
+        ref = capi.Solver(ctx, n, R, base_seed=77, params=p, trace_cap=16)
+        ref.run(race=False)
+        a = capi.Solver(ctx, n, R, base_seed=77, params=p, trace_cap=16)
+        a.run(epoch_iterations=4, race=False)
+        blob = a.save()
+        a.close()
+        b = capi.Solver(ctx, n, R, base_seed=77, params=p, trace_cap=16)
+        b.load(blob)
+        b.run(race=False)
+        ra, rb = ref.results(), b.results()
+        assert [(r["best"].tolist(), r["best_energy"], r["iterations"], r["trace"]) for r in ra] \
+            == [(r["best"].tolist(), r["best_energy"], r["iterations"], r["trace"]) for r in rb]
+        bad = capi.Solver(ctx, n + 1, R, base_seed=77, params=p, trace_cap=16)
+        with pytest.raises(ValueError):
+            bad.load(blob)
