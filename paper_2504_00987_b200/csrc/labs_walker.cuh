@@ -29,7 +29,7 @@
 // Shared layout per warp: C mirrored as C2[L + d] = C_{|d|} so the gather
 // C_{|j-p|} is one LDS at a per-step base + 128 b, double-buffered (a step
 // reads one buffer and writes the other); Q[m]; spins as a zero-padded int8
-// array S[L + x] so s_x for any x in (-L, 2L) is one LDS with the range check
+// array S[SO + x] so s_x for any x in (-L-4, 2L+4) is one LDS with the range check
 // folded into the padding. The flipped spin is stored by every lane at the
 // start of the next step (each lane then reads its own store), so a tabu
 // step needs a single warp barrier. Invalid lanes (j >= n) keep EX = INT_MAX
@@ -63,7 +63,8 @@ struct WalkSmem {
   static constexpr int L = 32 * NS;
   int32_t C2[2][2 * L];        // C2[buf][L + d] = C_{|d|}, d in (-L, L); 2 buffers
   int32_t Q[2 * L];            // Q[m], m in [0, 2n-1)
-  int8_t S[3 * L];             // spins (+1/-1), S[L + x]; 0 outside [0, n)
+  static constexpr int SO = L + 4;  // spin x lives at S[SO + x]
+  int8_t S[3 * L + 8];         // spins (+1/-1); 0 outside [0, n) (4 guard bytes)
   // Packed bit windows for the O(n^2/32) popcount build, aliased onto the
   // second C buffer (idle until the walk's first step): B32 holds s
   // (position x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
@@ -90,7 +91,7 @@ __device__ __forceinline__ uint32_t lowmask(int x) {
 // walk.
 template <int NS>
 __device__ __forceinline__ void smem_clear(WalkSmem<NS>& sm) {
-  for (int i = lane_id(); i < 3 * 32 * NS; i += 32) sm.S[i] = 0;
+  for (int i = lane_id(); i < 3 * 32 * NS + 8; i += 32) sm.S[i] = 0;
   __syncwarp();
 }
 
@@ -120,6 +121,7 @@ struct StepRec {      // mirrors labs_tabu_step (include/labs_b200.h)
 template <int NS>
 struct Walker {
   static constexpr int L = 32 * NS;
+  static constexpr int SO = WalkSmem<NS>::SO;
   WalkSmem<NS>* sm;
   int n;
   int H[NS], HQ[NS], MS[NS], EX[NS], CK[NS];
@@ -139,7 +141,7 @@ struct Walker {
       const int bit = ((in[b] & lowmask(n - 32 * b)) >> ln) & 1u;
       const int sp = j < n ? 1 - 2 * bit : 0;
       MS[b] = -sp;
-      s.S[L + j] = static_cast<int8_t>(sp);
+      s.S[SO + j] = static_cast<int8_t>(sp);
       EX[b] = j < n ? 0 : INT_MAX;
     }
     s.put_bits(n, in);
@@ -148,7 +150,7 @@ struct Walker {
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int i = 32 * b + ln;
-      const bool rb = i < n && s.S[L + n - 1 - i] < 0;
+      const bool rb = i < n && s.S[SO + n - 1 - i] < 0;
       const uint32_t m = __ballot_sync(kFull, rb);
       if (ln == 0) R32[NS + b] = m;
     }
@@ -209,13 +211,42 @@ struct Walker {
       h[b] = 0;
     }
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
-#pragma unroll 2
-    for (int k = 1; k < n; ++k) {
-      const int c = s.C2[0][L + k];
+    if constexpr (NS <= 4) {
+      // |C_k| <= 127: four lags per DP4A. C as int8 in the idle second C
+      // buffer (the bit windows are dead by now); spins read as 4-byte
+      // windows of S, the backward window byte-reversed.
+      int8_t* c8 = reinterpret_cast<int8_t*>(s.C2[1]);
+      for (int k = ln; k < L + 4; k += 32) c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[0][L + k] : 0);
+      __syncwarp();
+      const uint32_t* c8w = reinterpret_cast<const uint32_t*>(c8);
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(s.S);
 #pragma unroll
       for (int b = 0; b < NS; ++b) {
         const int j = 32 * b + ln;
-        h[b] += c * (static_cast<int>(s.S[L + j + k]) + static_cast<int>(s.S[L + j - k]));
+        const int fa = SO + j;          // byte of s_j (forward window start)
+        const int ba = SO + j - 3;      // byte of s_{j-3} (backward window start)
+        const uint32_t* fp = s32 + (fa >> 2);
+        const uint32_t* bp = s32 + (ba >> 2);
+        const int fsh = 8 * (fa & 3), bsh = 8 * (ba & 3);
+        int acc = 0;
+        for (int m = 0; 4 * m < n; ++m) {
+          const int cw = static_cast<int>(c8w[m]);
+          const int fw = static_cast<int>(__funnelshift_r(fp[m], fp[m + 1], fsh));
+          const uint32_t bw = __funnelshift_r(bp[-m], bp[-m + 1], bsh);
+          acc = __dp4a(cw, fw, acc);
+          acc = __dp4a(cw, static_cast<int>(__byte_perm(bw, 0u, 0x0123)), acc);
+        }
+        h[b] = acc;
+      }
+    } else {
+#pragma unroll 2
+      for (int k = 1; k < n; ++k) {
+        const int c = s.C2[0][L + k];
+#pragma unroll
+        for (int b = 0; b < NS; ++b) {
+          const int j = 32 * b + ln;
+          h[b] += c * (static_cast<int>(s.S[SO + j + k]) + static_cast<int>(s.S[SO + j - k]));
+        }
       }
     }
 #pragma unroll
@@ -231,9 +262,9 @@ struct Walker {
   // Spin store of the previous flip, performed by every lane before it reads
   // S (each lane then observes its own store).
   // (pend_pos = -1, pend_val = 0 after init rewrites the zero padding byte
-  // S[L-1], so the store needs no guard.)
+  // of position -1, so the store needs no guard.)
   __device__ __forceinline__ void flush_spin() {
-    sm->S[L + pend_pos] = static_cast<int8_t>(pend_val);
+    sm->S[SO + pend_pos] = static_cast<int8_t>(pend_val);
   }
 
   // Commit flip `pos` (warp-uniform); its expiry becomes t + tenure. Reads
@@ -244,15 +275,15 @@ struct Walker {
     const int ln = lane_id();
     WalkSmem<NS>& s = *sm;
     flush_spin();
-    const int sig = s.S[L + pos];
+    const int sig = s.S[SO + pos];
     const int c16 = sig * -16, c8 = sig * -8, c4 = sig * -4, c2 = sig * -2;
     const int32_t* cgp = &s.C2[cb][L + ln - pos];
     int32_t* cw = &s.C2[cb ^ 1][L];
     int32_t* qp = &s.Q[pos + ln];
-    const int8_t* s1p = &s.S[L + 2 * pos - ln];
-    const int8_t* s2p = &s.S[L + 2 * ln - pos];
-    const int8_t* smp = &s.S[L + pos - ln];
-    const int8_t* spp = &s.S[L + pos + ln];
+    const int8_t* s1p = &s.S[SO + 2 * pos - ln];
+    const int8_t* s2p = &s.S[SO + 2 * ln - pos];
+    const int8_t* smp = &s.S[SO + pos - ln];
+    const int8_t* spp = &s.S[SO + pos + ln];
     const int exp_new = t + tenure;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {

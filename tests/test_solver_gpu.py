@@ -139,3 +139,20 @@ def test_checkpoint_resume_is_exact(ctx):
         bad = capi.Solver(ctx, n + 1, R, base_seed=77, params=p, trace_cap=16)
         with pytest.raises(ValueError):
             bad.load(blob)
+
+
+def test_islands_driver_single_rank(ctx):
+    """islands.Islands on one GPU (world 1): epochs, elite exchange through
+    device buffers, stop on target."""
+    import torch
+    from paper_2504_00987_b200.islands import Islands
+    n, R = 40, 64
+    target = 108  # proven optimum (paper_2504_00987_b200/data/optima.txt)
+    sv = capi.Solver(ctx, n, R, base_seed=3, params=capi.memetic_params(
+        target_energy=target, max_seconds=120.0))
+    isl = Islands(sv, n, k_elites=4, device=torch.device("cuda", 0))
+    rep = isl.run(target=target, epoch_seconds=0.05, exchange_every=1, max_seconds=120.0)
+    assert rep.reached and rep.best_energy == target
+    assert rep.exchanges == rep.epochs and rep.epochs >= 1
+    best = sv.results()[rep.best_replica]
+    assert best["best_energy"] == target
