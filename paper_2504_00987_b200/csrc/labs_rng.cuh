@@ -254,7 +254,8 @@ __device__ __forceinline__ int uniform_below(R& rng, uint32_t r32) {
   uint64_t x = rng.next();
   uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
   uint64_t p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
-  if (static_cast<uint32_t>(p1) == 0 && static_cast<uint32_t>(p0) < r32) {
+  // low 64 bits of x * r below r needs the middle word to be zero: ~2^-32.
+  if (__builtin_expect(static_cast<uint32_t>(p1) == 0, 0) && static_cast<uint32_t>(p0) < r32) {
     const uint64_t range = r32;
     const uint64_t thr = (0ULL - range) % range;
     uint64_t low = (p1 << 32) | static_cast<uint32_t>(p0);

@@ -276,7 +276,8 @@ struct Walker {
     WalkSmem<NS>& s = *sm;
     flush_spin();
     const int sig = s.S[SO + pos];
-    const int c16 = sig * -16, c8 = sig * -8, c4 = sig * -4, c2 = sig * -2;
+    // -2 sigma, -4 sigma, -8 sigma, -16 sigma by doubling (no multiplies)
+    const int c2 = -(sig + sig), c4 = c2 + c2, c8 = c4 + c4, c16 = c8 + c8;
     const int32_t* cgp = &s.C2[cb][L + ln - pos];
     int32_t* cw = &s.C2[cb ^ 1][L];
     int32_t* qp = &s.Q[pos + ln];
@@ -296,7 +297,7 @@ struct Walker {
       const int smv = smp[-32 * b];
       const int spv = spp[32 * b];
       // j != p: H += 16 s_{2p-j} + 32 s_j + c16 C_{|j-p|} + c8 Q_{p+j}
-      const int hn = H[b] + 16 * s1 - 32 * MS[b] + c16 * cg + c8 * qg;
+      const int hn = H[b] + 16 * s1 - 32 * MS[b] + c8 * (cg + cg + qg);
       const int hp = H[b] + c2 * HQ[b];  // j == p: H -= 8 sigma (n-2+Q_2p)
       H[b] = isp ? hp : hn;
       if (!isp) {
