@@ -155,6 +155,19 @@ def main():
     mcases.append(dict(n=40, seed=9, target_energy=0, max_iterations=15, p_mutate=0.2,
                        min_tabu_factor=0.2, max_tabu_factor=0.5))
     mcases.append(dict(n=150, seed=3, target_energy=0, max_iterations=4, population_size=12))
+    # edge cases: tiny n, K = 2, p_comb in {0, 1}, p_mutate = 1, zero tenure,
+    # fallback-heavy tenure, aspiration-free long walks
+    mcases.append(dict(n=2, seed=1, target_energy=0, max_iterations=5, population_size=2))
+    mcases.append(dict(n=3, seed=2, target_energy=0, max_iterations=8, population_size=3))
+    mcases.append(dict(n=17, seed=3, target_energy=0, max_iterations=10, p_comb=0.0))
+    mcases.append(dict(n=17, seed=4, target_energy=0, max_iterations=10, p_comb=1.0,
+                       p_mutate=1.0))
+    mcases.append(dict(n=33, seed=5, target_energy=0, max_iterations=6, min_tabu_factor=0.0,
+                       max_tabu_factor=0.0))
+    mcases.append(dict(n=33, seed=6, target_energy=0, max_iterations=6, min_tabu_factor=0.9,
+                       max_tabu_factor=0.99))
+    mcases.append(dict(n=65, seed=7, target_energy=0, max_iterations=5, population_size=2,
+                       p_comb=0.5, p_mutate=0.05))
     mcases.append(dict(n=256, seed=4, target_energy=0, max_iterations=2, population_size=5))
     for c in mcases:
         c = dict(c)

@@ -156,3 +156,18 @@ def test_islands_driver_single_rank(ctx):
     assert rep.exchanges == rep.epochs and rep.epochs >= 1
     best = sv.results()[rep.best_replica]
     assert best["best_energy"] == target
+
+
+def test_more_replicas_than_resident_warps(ctx, oracle):
+    """Replicas beyond the resident capacity run in later waves of the same
+    persistent grid; each is still the reference trajectory of its seed."""
+    n = 20
+    cap = capi.Solver.capacity(ctx, n)
+    R = cap + 37
+    p = capi.memetic_params(target_energy=0, max_iterations=2)
+    best, per = ctx.run_replicas(n, R, 500, p)
+    for r in (0, 1, cap - 1, cap, R - 1):
+        want = oracle.memetic(n, 500 + r, max_iterations=2)
+        assert per[r]["best"].tolist() == want["best"]
+        assert per[r]["best_energy"] == want["best_energy"]
+    assert best["best_energy"] == min(x["best_energy"] for x in per)
