@@ -59,59 +59,82 @@ __device__ __forceinline__ int exh_flip(uint64_t& s, int n, int j, int (&C)[KMAX
   return e;
 }
 
-// Mode 0: per-thread minimum -> atomicMin(best). Mode 1: record every
-// sequence with E == *target (s_0 = +1 half) into out[0..cap), count in *cnt.
-// Mode 2: count strict local optima (every single flip strictly worse).
+// Pass 1: the minimum energy of every thread's block of Gray indices.
 template <int KMAX>
-__global__ void __launch_bounds__(128) k_exhaust(int n, int B, uint64_t blocks, int mode,
-                                                 unsigned long long* best, const int* target,
-                                                 uint64_t* out, unsigned long long cap,
-                                                 unsigned long long* cnt) {
+__global__ void __launch_bounds__(128) k_exhaust_min(int n, int B, uint64_t blocks,
+                                                     int* block_min) {
   const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= blocks) return;
   const uint64_t span = 1ULL << B;
   uint64_t s = gray_bits(t * span);
   int C[KMAX];
   int e = exh_build<KMAX>(s, n, C);
-  int local_min = e;
-  unsigned long long local_cnt = 0;
-  const int tgt = mode == 1 ? *target : 0;
+  int best = e;
+  for (uint64_t l = 1; l < span; ++l) {
+    e = exh_flip<KMAX>(s, n, __ffsll(static_cast<long long>(l)), C, e);
+    best = e < best ? e : best;
+  }
+  block_min[t] = best;
+}
+
+// Pass 2, over the few blocks whose minimum is the optimum: record every
+// sequence of those blocks with E == target.
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_exhaust_collect(int n, int B, const uint32_t* ids,
+                                                         int count, int target, uint64_t* out,
+                                                         unsigned long long cap,
+                                                         unsigned long long* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t span = 1ULL << B;
+  uint64_t s = gray_bits(static_cast<uint64_t>(ids[i]) * span);
+  int C[KMAX];
+  int e = exh_build<KMAX>(s, n, C);
   for (uint64_t l = 0;; ++l) {
-    if (mode == 0) {
-      local_min = e < local_min ? e : local_min;
-    } else if (mode == 1) {
-      if (e == tgt) {
-        const unsigned long long slot = atomicAdd(cnt, 1ULL);
-        if (slot < cap) out[slot] = s;
-      }
-    } else {
-      // strict local optimum: dE_j > 0 for every j (proj/src/oracle.cpp:119-129)
-      bool opt = true;
-      for (int j = 0; j < n && opt; ++j) {
-        const int sj = ((s >> j) & 1ULL) ? -1 : 1;
-        int de = 0;
-#pragma unroll
-        for (int k = 1; k < KMAX; ++k) {
-          if (k < n) {
-            int d = 0;
-            if (j - k >= 0) d += ((s >> (j - k)) & 1ULL) ? -1 : 1;
-            if (j + k < n) d += ((s >> (j + k)) & 1ULL) ? -1 : 1;
-            d *= -2 * sj;
-            de += d * (2 * C[k] + d);
-          }
-        }
-        opt = de > 0;
-      }
-      local_cnt += opt ? 1 : 0;
+    if (e == target) {
+      const unsigned long long slot = atomicAdd(cnt, 1ULL);
+      if (slot < cap) out[slot] = s;
     }
     if (l + 1 == span) break;
     e = exh_flip<KMAX>(s, n, __ffsll(static_cast<long long>(l + 1)), C, e);
   }
-  if (mode == 0) {
-    atomicMin(best, static_cast<unsigned long long>(local_min));
-  } else if (mode == 2) {
-    if (local_cnt) atomicAdd(cnt, local_cnt);
+}
+
+// Strict local optima (every single flip strictly worse) of every block
+// (proj/src/oracle.cpp:112-151).
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_local_optima(int n, int B, uint64_t blocks,
+                                                      unsigned long long* cnt) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= blocks) return;
+  const uint64_t span = 1ULL << B;
+  uint64_t s = gray_bits(t * span);
+  int C[KMAX];
+  int e = exh_build<KMAX>(s, n, C);
+  unsigned long long local = 0;
+  for (uint64_t l = 0;; ++l) {
+    bool opt = true;
+    for (int j = 0; j < n && opt; ++j) {
+      const int sj = ((s >> j) & 1ULL) ? -1 : 1;
+      int de = 0;
+#pragma unroll
+      for (int k = 1; k < KMAX; ++k) {
+        if (k < n) {
+          int d = 0;
+          if (j - k >= 0) d += ((s >> (j - k)) & 1ULL) ? -1 : 1;
+          if (j + k < n) d += ((s >> (j + k)) & 1ULL) ? -1 : 1;
+          d *= -2 * sj;
+          de += d * (2 * C[k] + d);
+        }
+      }
+      opt = de > 0;
+    }
+    local += opt ? 1 : 0;
+    if (l + 1 == span) break;
+    e = exh_flip<KMAX>(s, n, __ffsll(static_cast<long long>(l + 1)), C, e);
   }
+  (void)e;
+  if (local) atomicAdd(cnt, local);
 }
 
 }  // namespace labsk

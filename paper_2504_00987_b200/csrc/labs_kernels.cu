@@ -1366,19 +1366,19 @@ int dispatch_kmax(int n, F&& f) {
   return f(std::integral_constant<int, 64>{});
 }
 
-int exhaust_launch(labs_ctx* ctx, int n, int mode, unsigned long long* best, const int* target,
-                   uint64_t* out, unsigned long long cap, unsigned long long* cnt) {
+struct ExhaustShape {
+  int B;            // Gray-index bits walked per thread
+  uint64_t blocks;  // threads
+  unsigned grid;
+};
+
+ExhaustShape exhaust_shape(int n) {
   const int free_bits = n - 1;
-  const int B = free_bits > 18 ? free_bits - 18 : 0;  // >= 2^18 threads when possible
-  const uint64_t blocks = 1ULL << (free_bits - B);
-  const unsigned grid = static_cast<unsigned>((blocks + 127) / 128);
-  return dispatch_kmax(n, [&](auto km) -> int {
-    constexpr int KMAX = decltype(km)::value;
-    k_exhaust<KMAX><<<grid, 128, 0, ctx->stream>>>(n, B, blocks, mode, best, target, out, cap,
-                                                   cnt);
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
-  });
+  ExhaustShape sh;
+  sh.B = free_bits > 18 ? free_bits - 18 : 0;  // >= 2^18 threads when possible
+  sh.blocks = 1ULL << (free_bits - sh.B);
+  sh.grid = static_cast<unsigned>((sh.blocks + 127) / 128);
+  return sh;
 }
 
 }  // namespace
@@ -1390,31 +1390,46 @@ extern "C" int labs_exhaustive_optimum(labs_ctx* ctx, int n, int64_t* optimal_en
   if (n < 2 || n > 64)
     return fail(LABS_ERR_INVALID_ARGUMENT, "device exhaustive search needs 2 <= n <= 64");
   LABS_CUDA(cudaSetDevice(ctx->device));
-  DBuf best, tgt, out, cnt;
-  LABS_ALLOC(best, sizeof(unsigned long long));
-  LABS_ALLOC(tgt, sizeof(int));
+  const ExhaustShape sh = exhaust_shape(n);
+  DBuf mins, ids, out, cnt;
+  LABS_ALLOC(mins, sizeof(int) * sh.blocks);
   LABS_ALLOC(out, sizeof(uint64_t) * std::max<int64_t>(cap, 1));
   LABS_ALLOC(cnt, sizeof(unsigned long long));
-  LABS_CUDA(cudaMemsetAsync(best.p, 0xff, sizeof(unsigned long long), ctx->stream));
   LABS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
-  if (int rc = exhaust_launch(ctx, n, 0, best.as<unsigned long long>(), nullptr, nullptr, 0,
-                              nullptr))
-    return rc;
-  unsigned long long e = 0;
-  LABS_D2H(&e, best.p, sizeof(e));
+  // pass 1: per-block minima
+  int rc = dispatch_kmax(n, [&](auto km) -> int {
+    constexpr int KMAX = decltype(km)::value;
+    k_exhaust_min<KMAX><<<sh.grid, 128, 0, ctx->stream>>>(n, sh.B, sh.blocks, mins.as<int>());
+    LABS_CUDA(cudaGetLastError());
+    return LABS_OK;
+  });
+  if (rc) return rc;
+  std::vector<int> h(sh.blocks);
+  LABS_D2H(h.data(), mins.p, sizeof(int) * sh.blocks);
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  const int ti = static_cast<int>(e);
-  LABS_H2D(tgt.p, &ti, sizeof(int));
-  if (int rc = exhaust_launch(ctx, n, 1, nullptr, tgt.as<int>(), out.as<uint64_t>(),
-                              static_cast<unsigned long long>(cap),
-                              cnt.as<unsigned long long>()))
-    return rc;
+  const int e = *std::min_element(h.begin(), h.end());
+  std::vector<uint32_t> sel;
+  for (uint64_t t = 0; t < sh.blocks; ++t)
+    if (h[t] == e) sel.push_back(static_cast<uint32_t>(t));
+  // pass 2: witnesses, only in the blocks that hold the optimum
+  LABS_ALLOC(ids, sizeof(uint32_t) * sel.size());
+  LABS_H2D(ids.p, sel.data(), sizeof(uint32_t) * sel.size());
+  rc = dispatch_kmax(n, [&](auto km) -> int {
+    constexpr int KMAX = decltype(km)::value;
+    const int cntb = static_cast<int>(sel.size());
+    k_exhaust_collect<KMAX><<<(cntb + 127) / 128, 128, 0, ctx->stream>>>(
+        n, sh.B, ids.as<uint32_t>(), cntb, e, out.as<uint64_t>(),
+        static_cast<unsigned long long>(cap), cnt.as<unsigned long long>());
+    LABS_CUDA(cudaGetLastError());
+    return LABS_OK;
+  });
+  if (rc) return rc;
   unsigned long long c = 0;
   LABS_D2H(&c, cnt.p, sizeof(c));
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (cap && c) LABS_D2H(witnesses, out.p, sizeof(uint64_t) * std::min<uint64_t>(c, cap));
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  *optimal_energy = static_cast<int64_t>(e);
+  *optimal_energy = e;
   *count = static_cast<int64_t>(c);
   return LABS_OK;
 }
@@ -1427,9 +1442,15 @@ extern "C" int labs_local_optima(labs_ctx* ctx, int n, int64_t* count) {
   DBuf cnt;
   LABS_ALLOC(cnt, sizeof(unsigned long long));
   LABS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
-  if (int rc = exhaust_launch(ctx, n, 2, nullptr, nullptr, nullptr, 0,
-                              cnt.as<unsigned long long>()))
-    return rc;
+  const ExhaustShape sh = exhaust_shape(n);
+  int rc = dispatch_kmax(n, [&](auto km) -> int {
+    constexpr int KMAX = decltype(km)::value;
+    k_local_optima<KMAX><<<sh.grid, 128, 0, ctx->stream>>>(n, sh.B, sh.blocks,
+                                                           cnt.as<unsigned long long>());
+    LABS_CUDA(cudaGetLastError());
+    return LABS_OK;
+  });
+  if (rc) return rc;
   unsigned long long c = 0;
   LABS_D2H(&c, cnt.p, sizeof(c));
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
