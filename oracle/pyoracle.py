@@ -263,6 +263,17 @@ class Reference:
         L.ref_brute_force.restype = C.c_int
         L.ref_local_optima.argtypes = [C.c_int, C.c_int]
         L.ref_local_optima.restype = C.c_int64
+        L.ref_deviation.argtypes = [C.c_int, u64p, C.c_uint64, C.c_int, i64p]
+        L.ref_deviation.restype = C.c_int
+
+    def deviation(self, n, words, budget=0, edits=False):
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        out = np.zeros(3, dtype=np.int64)
+        if self.lib.ref_deviation(n, _p(w, u64p), C.c_uint64(budget), 1 if edits else 0,
+                                  _p(out, i64p)) != 0:
+            raise ValueError("deviation failed")
+        return {"value": int(out[0]), "budget_exceeded": bool(out[1]),
+                "evaluations": int(out[2])}
 
     def brute_force(self, n, workers=8, cap=4096):
         e = C.c_int64(0)

@@ -22,6 +22,7 @@
 #include "labsolve/parallel.hpp"
 #include "labsolve/rng.hpp"
 #include "labsolve/sequence.hpp"
+#include "labsolve/skew.hpp"
 #include "labsolve/tabu.hpp"
 
 using namespace labsolve;
@@ -229,6 +230,21 @@ int ref_brute_force(int n, int workers, int64_t* energy, uint64_t* witnesses, in
 int64_t ref_local_optima(int n, int workers) {
   try {
     return enumerate_local_optima(n, workers);
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// deviation / deviation_with_edits (skew.cpp:110-187): out = {value,
+// budget_exceeded, evaluations}.
+int ref_deviation(int n, const uint64_t* w, uint64_t budget, int edits, int64_t* out) {
+  try {
+    DeviationResult d = edits ? deviation_with_edits(from_words(n, w), budget)
+                              : deviation(from_words(n, w), budget);
+    out[0] = d.value;
+    out[1] = d.budget_exceeded ? 1 : 0;
+    out[2] = static_cast<int64_t>(d.evaluations);
+    return 0;
   } catch (const std::exception&) {
     return -1;
   }

@@ -1,12 +1,14 @@
 // labsolve exhaustive ground truth on the B200 (oracle.hpp).
 #include "labsolve/oracle.hpp"
 
+#include <cmath>
 #include <fstream>
 #include <set>
 #include <sstream>
 #include <stdexcept>
 
 #include "device.hpp"
+#include "labsolve/skew.hpp"
 
 namespace labsolve {
 
@@ -66,6 +68,35 @@ std::vector<TableEntry> read_table_file(const std::string& path) {
     out.push_back(e);
   }
   return out;
+}
+
+// verify_published (oracle.cpp:174-199): energy, merit within 0.005, skew
+// deviation under the budget; a row that fails to decode records the error
+// and the run continues.
+VerifyReport verify_published(const std::vector<TableEntry>& entries,
+                              std::uint64_t deviation_budget) {
+  VerifyReport rep;
+  rep.all_pass = true;
+  for (const TableEntry& want : entries) {
+    VerifyEntry v;
+    v.expected = want;
+    try {
+      const Sequence s = decode_hex(want.hex, want.n);
+      v.energy = energy(s);
+      v.merit = merit_factor(want.n, v.energy);
+      const DeviationResult d = deviation(s, deviation_budget);
+      v.deviation = d.value;
+      v.budget_exceeded = d.budget_exceeded;
+      v.energy_ok = v.energy == want.energy;
+      v.merit_ok = std::fabs(v.merit - want.merit) <= 0.005;
+      v.deviation_ok = !d.budget_exceeded && d.value == want.deviation;
+    } catch (const std::exception& e) {
+      v.error = e.what();
+    }
+    rep.all_pass = rep.all_pass && v.pass();
+    rep.entries.push_back(v);
+  }
+  return rep;
 }
 
 }  // namespace labsolve

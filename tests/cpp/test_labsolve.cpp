@@ -238,7 +238,16 @@ static void parallel() {
   CHECK_THROWS_AS(run_replicas(broken), std::invalid_argument);
 }
 
+static std::string g_table = "tests/golden/table2.txt";
+
 static void oracle() {
+  // verify_published over Table II: energy on device, MF, skew deviation
+  std::vector<TableEntry> rows = read_table_file(g_table);
+  CHECK(rows.size() == 17);
+  VerifyReport rep = verify_published(rows);
+  CHECK(rep.all_pass);
+  VerifyReport capped = verify_published({rows.front()}, 10);
+  CHECK(!capped.all_pass && capped.entries[0].budget_exceeded);
   BruteForceResult r = brute_force_optimum(13, 4);
   CHECK(r.optimal_energy == 6 && r.witnesses.size() == 1);
   CHECK(encode_hex(r.witnesses[0]) == "0650");  // README.md:102-104
@@ -252,7 +261,8 @@ static void oracle() {
   CHECK(res.energy == 6);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) g_table = argv[1];
   sequences();
   oracle();
   correlation();

@@ -195,7 +195,22 @@ def main():
         exhaustive.append({"n": n, "E": e, "witnesses": [encode_hex(x, n) for x in w]})
     local_optima = {n: ref.local_optima(n) for n in range(3, 21)}
 
-    fixtures = {"rng": rng_cases, "exhaustive": exhaustive, "local_optima": local_optima, "kats": kats, "table": table, "targets": targets,
+    # 9. Skew deviation d(S) (skew.cpp:110-187): the Table II rows and random
+    # short sequences, plain and with edits, with and without budgets.
+    skew = []
+    for row in table:
+        w = decode_hex(row["hex"], row["n"])
+        skew.append({"n": row["n"], "words": words_list(w), "budget": 0, "edits": False,
+                     **ref.deviation(row["n"], w)})
+    for i in range(24):
+        n = int(rs.integers(3, 40))
+        w = ref.random_sequences(n, 9000 + i, 1)[0]
+        for edits in (False, True):
+            for budget in (0, int(rs.integers(1, 60))):
+                skew.append({"n": n, "words": words_list(w), "budget": budget, "edits": edits,
+                             **ref.deviation(n, w, budget, edits)})
+
+    fixtures = {"rng": rng_cases, "skew": skew, "exhaustive": exhaustive, "local_optima": local_optima, "kats": kats, "table": table, "targets": targets,
                 "targets_small": small, "probes": probes, "scans": scans, "walks": walks,
                 "memetic": memetic, "replicas": replicas}
     for item in replicas:
@@ -204,6 +219,10 @@ def main():
             rr.pop("wall_seconds", None)
     for item in memetic:
         item["best"] = [int(x) for x in item["best"]]
+    with open(os.path.join(OUT, "table2.txt"), "w") as f:
+        f.write("# Table II rows (proj/data/published_sequences.txt): n hex E MF d\n")
+        for row in table:
+            f.write(f'{row["n"]} {row["hex"]} {row["E"]} {row["mf"]} {row["d"]}\n')
     path = os.path.join(OUT, "reference_vectors.json")
     with open(path, "w") as f:
         json.dump(fixtures, f, separators=(",", ":"))

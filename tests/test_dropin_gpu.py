@@ -13,7 +13,8 @@ BIN = os.path.join(ROOT, "tests", "cpp", "test_labsolve")
 @pytest.mark.gpu
 def test_cpp_dropin_suite():
     assert os.path.exists(BIN), "build with __graft_entry__.build() (make -C tests/cpp)"
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([BIN, os.path.join(ROOT, "tests", "golden", "table2.txt")],
+                       capture_output=True, text=True, timeout=600)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
     assert "0 failed" in r.stdout

@@ -1,0 +1,29 @@
+"""skew.hpp drop-in (deviation from skew-symmetry, host analysis) against the
+reference's own deviation / deviation_with_edits, including budgets and
+evaluation counts, and the Table II d(S) column."""
+import os
+import subprocess
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def test_deviation_matches_reference(golden):
+    exe = os.path.join(ROOT, "tests", "cpp", "skew_probe")
+    assert os.path.exists(exe), "build with __graft_entry__.build()"
+    cases = golden["skew"]
+    stdin = "\n".join(f'{c["n"]} {c["budget"]} {int(c["edits"])} ' +
+                      " ".join(str(w) for w in c["words"]) for c in cases) + "\n"
+    r = subprocess.run([exe], input=stdin, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    got = [tuple(int(x) for x in line.split()) for line in r.stdout.splitlines()]
+    want = [(c["value"], int(c["budget_exceeded"]), c["evaluations"]) for c in cases]
+    assert got == want
+
+
+def test_table_deviation_column(golden):
+    by = {(c["n"], tuple(c["words"])): c["value"] for c in golden["skew"] if not c["edits"]
+          and c["budget"] == 0}
+    from paper_2504_00987_b200.sequence import decode_hex
+    for row in golden["table"]:
+        key = (row["n"], tuple(int(x) for x in decode_hex(row["hex"], row["n"])))
+        assert by[key] == row["d"]
