@@ -293,7 +293,10 @@ def main():
     solver.close()
 
     if rank == 0 and world == 1 and not args.quick:
-        line["cpu_baseline"] = cpu_reference_throughput(n, args.cpu_seconds)
+        try:
+            line["cpu_baseline"] = cpu_reference_throughput(n, args.cpu_seconds)
+        except Exception as e:  # the checker library was not built on this host
+            line["cpu_baseline"] = {"unavailable": f"{type(e).__name__}: {e}"}
         if n in TARGETS and args.tts_seeds > 0:
             line["tts"] = time_to_target(ctx, capi, n, TARGETS[n], R, rng_kind, args)
     if rank == 0:
