@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-end evidence on one B200 (run under gpurun from the repo root):
+#   1. the bench line (no profiler),
+#   2. the launch list of the same command (gpu__time_duration per launch),
+#   3. one full ncu capture of the bench kernel (k_memetic, N=64).
+# Each ncu pass follows a plain run of the same command that exited 0.
+set -e
+mkdir -p gpurun_out
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench_final.log 2>&1
+tail -1 gpurun_out/bench_final.log
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_final.csv python bench.py --steps 10 --warmup 3 \
+    > gpurun_out/ncu_launches.log 2>&1
+python bench.py --quick --steps 1 --warmup 1 --epoch-ms 20 > gpurun_out/plain.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_memetic -s 1 -c 1 \
+    -o gpurun_out/prof_final python bench.py --quick --steps 1 --warmup 1 --epoch-ms 20 \
+    > gpurun_out/ncu_full.log 2>&1
+echo profile_round done
