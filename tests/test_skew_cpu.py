@@ -27,3 +27,20 @@ def test_table_deviation_column(golden):
     for row in golden["table"]:
         key = (row["n"], tuple(int(x) for x in decode_hex(row["hex"], row["n"])))
         assert by[key] == row["d"]
+
+
+def test_host_rng_matches_reference(golden):
+    """labsolve::Rng (host side of the drop-in) against the reference's draws."""
+    exe = os.path.join(ROOT, "tests", "cpp", "rng_probe")
+    assert os.path.exists(exe), "build with __graft_entry__.build()"
+    lines = []
+    for c in golden["rng"]:
+        parts = [str(c["seed"]), str(len(c["kinds"]))]
+        for k, lo, hi in zip(c["kinds"], c["lo"], c["hi"]):
+            parts += [str(k), str(lo), str(hi)]
+        lines.append(" ".join(parts))
+    r = subprocess.run([exe], input="\n".join(lines) + "\n", capture_output=True, text=True,
+                       timeout=60)
+    assert r.returncode == 0, r.stderr
+    got = [[int(x) for x in line.split()] for line in r.stdout.splitlines()]
+    assert got == [c["out"] for c in golden["rng"]]
