@@ -292,11 +292,10 @@ struct Walker {
     const int8_t* smp = &s.S[SO + pos - ln];
     const int8_t* spp = &s.S[SO + pos + ln];
     const int exp_new = t + tenure;
-    const int dpl = pos - ln;  // slot b holds the flip iff dpl == 32 b
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = 32 * b + ln;
-      const bool isp = dpl == 32 * b;
+      const bool isp = j == pos;
       const int cg = cgp[32 * b];
       const int qg = qp[32 * b];
       const int s1 = s1p[-32 * b];
