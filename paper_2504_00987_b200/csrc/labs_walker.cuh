@@ -56,12 +56,6 @@ __device__ __forceinline__ int warp_min(int v) {
   return r;
 }
 
-__device__ __forceinline__ int warp_sum(int v) {
-  int r;
-  asm volatile("redux.sync.add.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
-  return r;
-}
-
 __device__ __forceinline__ uint32_t lowmask(int x);
 
 template <int NS>
@@ -407,12 +401,11 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
 #if LABS_TIE_DUAL
     tied = (255 - (kmin_hi & 255)) != pos;
 #else
-    // every key of the minimal dE lies in [kmin, kmin | 255]; count them
-    const int lim = kmin | 255;
-    int c = 0;
+    int k2 = INT_MAX;
 #pragma unroll
-    for (int b = 0; b < NS; ++b) c += key[b] <= lim;
-    tied = warp_sum(c) > 1;
+    for (int b = 0; b < NS; ++b) k2 = min(k2, key[b] == kmin ? INT_MAX : key[b]);
+    k2 = warp_min(k2);
+    tied = (k2 >> 8) == dmin;
 #endif
   }
   ntie = 1;
