@@ -38,11 +38,18 @@
 #pragma once
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "labs_rng.cuh"
 
 #ifndef LABS_TIE_DUAL
 #define LABS_TIE_DUAL 0
+#endif
+#ifndef LABS_HN4
+#define LABS_HN4 0
+#endif
+#ifndef LABS_HQ_SEL
+#define LABS_HQ_SEL 0
 #endif
 
 namespace labsk {
@@ -272,14 +279,22 @@ struct Walker {
   // and written by lane j alone); one warp barrier orders this step's stores
   // before the next step's loads.
   __device__ __forceinline__ void apply(int pos, int dEp, int t, int tenure) {
+    if (cb) apply_cb<1>(pos, dEp, t, tenure);
+    else apply_cb<0>(pos, dEp, t, tenure);
+  }
+
+  // apply() with the C buffer index known at compile time (the tabu loop is
+  // unrolled by two so the buffers alternate statically).
+  template <int CB>
+  __device__ __forceinline__ void apply_cb(int pos, int dEp, int t, int tenure) {
     const int ln = lane_id();
     WalkSmem<NS>& s = *sm;
     flush_spin();
     const int sig = s.S[SO + pos];
     // -2 sigma, -4 sigma, -8 sigma, -16 sigma by doubling (no multiplies)
     const int c2 = -(sig + sig), c4 = c2 + c2, c8 = c4 + c4, c16 = c8 + c8;
-    const int32_t* cgp = &s.C2[cb][L + ln - pos];
-    int32_t* cw = &s.C2[cb ^ 1][L];
+    const int32_t* cgp = &s.C2[CB][L + ln - pos];
+    int32_t* cw = &s.C2[CB ^ 1][L];
     int32_t* qp = &s.Q[pos + ln];
     const int8_t* s1p = &s.S[SO + 2 * pos - ln];
     const int8_t* s2p = &s.S[SO + 2 * ln - pos];
@@ -297,20 +312,29 @@ struct Walker {
       const int smv = smp[-32 * b];
       const int spv = spp[32 * b];
       // j != p: H += 16 s_{2p-j} + 32 s_j + c16 C_{|j-p|} + c8 Q_{p+j}
+#if LABS_HN4
+      const int hn = H[b] + 16 * (s1 - 2 * MS[b]) + c8 * (cg + cg + qg);
+#else
       const int hn = H[b] + 16 * s1 - 32 * MS[b] + c8 * (cg + cg + qg);
+#endif
       const int hp = H[b] + c2 * HQ[b];  // j == p: H -= 8 sigma (n-2+Q_2p)
       H[b] = isp ? hp : hn;
+#if LABS_HQ_SEL
+      if (!isp) qp[32 * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
+      HQ[b] += isp ? 0 : c16 * s2;             // Q_{2j}  -= 4 sigma s_{2j-p}
+#else
       if (!isp) {
         qp[32 * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
         HQ[b] += c16 * s2;             // Q_{2j}  -= 4 sigma s_{2j-p}
       }
+#endif
       CK[b] += c2 * (smv + spv);       // C_j -= 2 sigma (s_{p-j} + s_{p+j})
       cw[j] = CK[b];
       cw[-j] = CK[b];
       MS[b] = isp ? -MS[b] : MS[b];
       EX[b] = isp ? exp_new : EX[b];
     }
-    cb ^= 1;
+    cb = CB ^ 1;
     pend_pos = pos;
     pend_val = -sig;
     E += dEp;
@@ -453,7 +477,7 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
   const uint32_t tenure_range = static_cast<uint32_t>(max_t - min_t + 1);
 #pragma unroll
   for (int b = 0; b < NS; ++b) best[b] = in[b] & lowmask(n - 32 * b);
-  for (int t = 1; t <= m; ++t) {
+  auto step = [&](auto cbc, int t) {
     int dE[NS];
     bool adm[NS];
     w.delta(dE);
@@ -471,7 +495,7 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
     uint32_t msk[NS];
     select_move<NS, false>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
     const int tenure = min_t + uniform_below(rng, tenure_range);
-    w.apply(pos, dEp, t, tenure);
+    w.template apply_cb<decltype(cbc)::value>(pos, dEp, t, tenure);
     if (w.E < bestE) {
       bestE = w.E;
       w.chunks(best);
@@ -485,6 +509,12 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
       rec.fallback = fb;
       trace[t - 1] = rec;
     }
+  };
+  // Unrolled by two: even steps read C buffer 0, odd steps buffer 1.
+  for (int t = 1; t <= m; t += 2) {
+    step(std::integral_constant<int, 0>{}, t);
+    if (t + 1 > m) break;
+    step(std::integral_constant<int, 1>{}, t + 1);
   }
   if (steps_out) *steps_out = m;
   return bestE;
