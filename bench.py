@@ -244,11 +244,14 @@ def main():
         except Exception:
             traffic = None
 
-    # e2e through the reference-facing C-ABI call with host buffers
-    e2e_iters = 2000
-    e2e_params = capi.memetic_params(target_energy=0, max_iterations=e2e_iters,
+    # e2e through the reference-facing C-ABI call with host buffers: a solve
+    # with a wall budget (`labs solve --time-limit`), so every replica works
+    # until the budget and none idles at the end of the call.
+    e2e_budget = 0.5
+    e2e_params = capi.memetic_params(target_energy=0, max_seconds=e2e_budget,
                                      rng_kind=rng_kind)
-    ctx.run_replicas(n, R, 7, e2e_params)  # warm
+    ctx.run_replicas(n, R, 7, capi.memetic_params(target_energy=0, max_iterations=2,
+                                                  rng_kind=rng_kind))  # warm
     t0 = time.perf_counter()
     best, per = ctx.run_replicas(n, R, 1000 + rank * R, e2e_params)
     e2e_t = time.perf_counter() - t0
@@ -287,7 +290,7 @@ def main():
                      "issue_slots_busy_ncu": issue},
         "e2e": {"value": e2e_value, "unit": "flip-evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "call": f"labs_run_replicas(n={n}, replicas={R}, max_iterations={e2e_iters})"},
+                "call": f"labs_run_replicas(n={n}, replicas={R}, max_seconds={e2e_budget})"},
         "clocks": clocks.summary(),
     }
     solver.close()
