@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -40,23 +41,37 @@ __host__ __device__ constexpr int min_blocks() {
   return NS <= 4 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
 }
 
-template <int NS, bool MT>
-struct WarpSlot {
+// Shared memory of one walker (tile): RNG block, cold replica bookkeeping,
+// walker vectors.
+template <int L, bool MT>
+struct TileSlot {
   uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
   uint64_t out[MT ? kMtN : PhiloxRng::kBlock];  // tempered block / Philox block
-  WalkSmem<NS> walk;
+  TileCtl ctl;
+  WalkSmemL<L> walk;
 };
 
-template <int NS, bool MT>
-__host__ __device__ constexpr size_t slot_bytes() {
-  return (sizeof(WarpSlot<NS, MT>) + 15) & ~size_t(15);
+template <int L, bool MT>
+__host__ __device__ constexpr size_t tile_slot_bytes() {
+  return (sizeof(TileSlot<L, MT>) + 15) & ~size_t(15);
+}
+
+// Tile t of the block owns slot t; T = 32 is the warp-per-walker kernels'.
+template <int L, bool MT, int T>
+__device__ __forceinline__ TileSlot<L, MT>& my_tile_slot() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return *reinterpret_cast<TileSlot<L, MT>*>(smem_raw +
+                                             (threadIdx.x / T) * tile_slot_bytes<L, MT>());
 }
 
 template <int NS, bool MT>
-__device__ __forceinline__ WarpSlot<NS, MT>& my_slot() {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  return *reinterpret_cast<WarpSlot<NS, MT>*>(smem_raw +
-                                              (threadIdx.x >> 5) * slot_bytes<NS, MT>());
+__host__ __device__ constexpr size_t slot_bytes() {
+  return tile_slot_bytes<32 * NS, MT>();
+}
+
+template <int NS, bool MT>
+__device__ __forceinline__ TileSlot<32 * NS, MT>& my_slot() {
+  return my_tile_slot<32 * NS, MT, 32>();
 }
 
 __device__ __forceinline__ int global_warp() {
@@ -64,19 +79,22 @@ __device__ __forceinline__ int global_warp() {
 }
 __device__ __forceinline__ int total_warps() { return gridDim.x * kWarps; }
 
-// Load an engine state into the warp's slot and bind `rng` to it.
+// Load an engine state into the tile's slot and bind `rng` to it.
+template <int T = 32>
 __device__ __forceinline__ void mt_load(uint64_t* s, uint64_t* out, const labs_rng_state& g,
-                                        MtRng& rng) {
-  for (int i = lane_id(); i < kMtN; i += 32) s[i] = g.mt[i];
-  __syncwarp();
-  mt_temper_all(s, out);
+                                        MtRngT<T>& rng) {
+  for (int i = tile_lane<T>(); i < kMtN; i += T) s[i] = g.mt[i];
+  tile_sync<T>();
+  mt_temper_all<T>(s, out);
   rng.bind(s, out, g.idx);
 }
+template <int T = 32>
 __device__ __forceinline__ void mt_store(const uint64_t* s, labs_rng_state& g,
                                          int idx) {
-  __syncwarp();
-  for (int i = lane_id(); i < kMtN; i += 32) g.mt[i] = s[i];
-  if (lane_id() == 0) g.idx = idx;
+  tile_sync<T>();
+  for (int i = tile_lane<T>(); i < kMtN; i += T) g.mt[i] = s[i];
+  if (tile_lane<T>() == 0) g.idx = idx;
+  tile_sync<T>();
 }
 
 // ------------------------------------------------------------------ K1 --
@@ -178,7 +196,7 @@ k_scan(int n, int count, const uint64_t* __restrict__ words,
 #pragma unroll
     for (int b = 0; b < NS; ++b) msk[b] = 0u;
     if (any || allow_fallback)
-      select_move<NS, true>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
+      select_move<NS, 32, true>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
     if (lane_id() == 0) {
       pos_out[item] = pos;
       e_out[item] = pos >= 0 ? static_cast<int64_t>(w.E) + dEp : 0;
@@ -280,30 +298,63 @@ __global__ void k_seed(int count, uint64_t base, labs_rng_state* out) {
 }
 
 // ------------------------------------------------------------------ K4 --
-template <int NS, bool MT>
-__global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_memetic(MemeticArgs A) {
-  auto& sl = my_slot<NS, MT>();
-  smem_clear(sl.walk);
-  Walker<NS> w;
+// Replica RNG binding for memetic_tiles: mt19937_64 state copied between the
+// replica's global record and the tile's shared slot, or the Philox stream
+// (key = base seed, stream = global replica id) positioned at its counter.
+template <int T>
+struct MtBind {
+  labs_rng_state* g;
+  uint64_t* mt;
+  uint64_t* out;
+  __device__ __forceinline__ void load(int r, MtRngT<T>& rng) { mt_load<T>(mt, out, g[r], rng); }
+  __device__ __forceinline__ void save(int r, MtRngT<T>& rng) { mt_store<T>(mt, g[r], rng.idx); }
+};
+template <int T>
+struct PhiloxBind {
+  uint64_t* ctr;
+  uint64_t* buf;
+  int64_t offset;
+  __device__ __forceinline__ void load(int r, PhiloxRngT<T>& rng) {
+    rng.s0 = static_cast<uint32_t>(offset + r);
+    rng.bind(buf, ctr[r]);
+  }
+  __device__ __forceinline__ void save(int r, PhiloxRngT<T>& rng) {
+    if (tile_lane<T>() == 0) ctr[r] = rng.ctr;
+    tile_sync<T>();
+  }
+};
+
+// Replicas per tile of T lanes; T < 32 packs 32/T replicas into each warp
+// (labs_memetic.cuh: memetic_tiles).
+template <int NS, int T>
+__host__ __device__ constexpr int min_blocks_memetic() {
+  return T * NS <= 128 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
+}
+
+template <int NS, int T, bool MT>
+__global__ void __launch_bounds__(32 * kWarps, (min_blocks_memetic<NS, T>()))
+k_memetic(MemeticArgs A) {
+  constexpr int L = T * NS;
+  auto& sl = my_tile_slot<L, MT, T>();
+  smem_clear<L, T>(sl.walk);
+  Walker<NS, T> w;
   w.sm = &sl.walk;
-  for (int r = global_warp(); r < A.replicas; r += total_warps()) {
-    if (A.initialized[r] && A.status[r] != kRunning) continue;
-    if constexpr (MT) {
-      MtRng rng;
-      mt_load(sl.mt, sl.out, A.mt[r], rng);
-      memetic_replica<NS>(A, r, w, rng);
-      mt_store(sl.mt, A.mt[r], rng.idx);
-    } else {
-      PhiloxRng rng;
-      rng.k0 = static_cast<uint32_t>(A.base_seed);
-      rng.k1 = static_cast<uint32_t>(A.base_seed >> 32);
-      rng.s0 = static_cast<uint32_t>(A.replica_offset + r);
-      rng.s1 = 0x4D454D45u;  // "MEME"
-      rng.bind(sl.out, A.ctr[r]);
-      memetic_replica<NS>(A, r, w, rng);
-      if (lane_id() == 0) A.ctr[r] = rng.ctr;
-    }
-    __syncwarp();
+  if constexpr (MT) {
+    MtRngT<T> rng;
+    rng.bind(sl.mt, sl.out, 0);  // valid until a replica is loaded
+    MtBind<T> rb{A.mt, sl.mt, sl.out};
+    if (A.tabu.aspiration) memetic_tiles<NS, T, true>(A, w, rng, rb, sl.ctl);
+    else memetic_tiles<NS, T, false>(A, w, rng, rb, sl.ctl);
+  } else {
+    PhiloxRngT<T> rng;
+    rng.k0 = static_cast<uint32_t>(A.base_seed);
+    rng.k1 = static_cast<uint32_t>(A.base_seed >> 32);
+    rng.s0 = 0;
+    rng.s1 = 0x4D454D45u;  // "MEME"
+    rng.bind(sl.out, 0);  // valid until a replica is loaded
+    PhiloxBind<T> rb{A.ctr, sl.out, A.replica_offset};
+    if (A.tabu.aspiration) memetic_tiles<NS, T, true>(A, w, rng, rb, sl.ctl);
+    else memetic_tiles<NS, T, false>(A, w, rng, rb, sl.ctl);
   }
 }
 
@@ -468,11 +519,12 @@ struct DBuf {
   LABS_CUDA(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, ctx->stream))
 
 template <class Kern>
-int grid_for(labs_ctx* ctx, Kern kern, size_t smem, int items, int* grid) {
+int grid_for(labs_ctx* ctx, Kern kern, size_t smem, int items, int* grid,
+             int per_block = kWarps) {
   int per_sm = 0;
   LABS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kWarps, smem));
   if (per_sm < 1) per_sm = 1;
-  const int want = (items + kWarps - 1) / kWarps;
+  const int want = (items + per_block - 1) / per_block;
   *grid = std::max(1, std::min(want, per_sm * ctx->sm_count));
   return LABS_OK;
 }
@@ -854,13 +906,38 @@ int check_memetic(int n, const labs_memetic_params* p) {
   return check_tabu(&p->tabu);
 }
 
-template <int NS, bool MT>
+// Memetic kernel shape: one replica per warp (T = 32) by default;
+// LABS_TILE=16 in the environment packs two replicas of n <= 64 into each
+// warp (16-lane tiles, 2 or 4 slots per lane). Measured on B200 at n = 64:
+// the 16-lane form issues ~10% fewer instructions per walker-step but loses
+// more to bank conflicts between the two tiles' slots and to L0 I-cache
+// misses (optimization log), so it is an option, not the default.
+bool memetic_tiled(int n) {
+  const char* e = std::getenv("LABS_TILE");
+  return n <= 64 && e && std::atoi(e) == 16;
+}
+
+template <class F>
+int dispatch_memetic(int n, F&& f) {
+  if (memetic_tiled(n)) {
+    if (n <= 32) return f(std::integral_constant<int, 2>{}, std::integral_constant<int, 16>{});
+    return f(std::integral_constant<int, 4>{}, std::integral_constant<int, 16>{});
+  }
+  return dispatch(n, [&](auto ns) -> int { return f(ns, std::integral_constant<int, 32>{}); });
+}
+
+template <int NS, int T, bool MT>
+constexpr size_t memetic_smem() {
+  return (32 / T) * kWarps * tile_slot_bytes<T * NS, MT>();
+}
+
+template <int NS, int T, bool MT>
 int launch_memetic(labs_ctx* ctx, const MemeticArgs& A) {
-  const size_t smem = kWarps * slot_bytes<NS, MT>();
-  auto kern = k_memetic<NS, MT>;
+  const size_t smem = memetic_smem<NS, T, MT>();
+  auto kern = k_memetic<NS, T, MT>;
   if (int r = prep(kern, smem)) return r;
   int grid = 0;
-  if (int r = grid_for(ctx, kern, smem, A.replicas, &grid)) return r;
+  if (int r = grid_for(ctx, kern, smem, A.replicas, &grid, kWarps * (32 / T))) return r;
   kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
   LABS_CUDA(cudaGetLastError());
   return LABS_OK;
@@ -888,16 +965,19 @@ int labs_solver_capacity(labs_ctx* ctx, int n, int rng_kind) {
   if (!ctx || check_n(n)) return 0;
   int out = 0;
   cudaSetDevice(ctx->device);
-  dispatch(n, [&](auto ns) -> int {
-    constexpr int NS = decltype(ns)::value;
+  dispatch_memetic(n, [&](auto ns, auto tt) -> int {
+    constexpr int NS = decltype(ns)::value, T = decltype(tt)::value;
     int per_sm = 0;
-    if (rng_kind == LABS_RNG_MT19937_64)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, true>, 32 * kWarps,
-                                                    kWarps * slot_bytes<NS, true>());
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, false>, 32 * kWarps,
-                                                    kWarps * slot_bytes<NS, false>());
-    out = per_sm * ctx->sm_count * kWarps;
+    if (rng_kind == LABS_RNG_MT19937_64) {
+      if (prep(k_memetic<NS, T, true>, memetic_smem<NS, T, true>())) return LABS_OK;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, T, true>, 32 * kWarps,
+                                                    memetic_smem<NS, T, true>());
+    } else {
+      if (prep(k_memetic<NS, T, false>, memetic_smem<NS, T, false>())) return LABS_OK;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, T, false>, 32 * kWarps,
+                                                    memetic_smem<NS, T, false>());
+    }
+    out = per_sm * ctx->sm_count * kWarps * (32 / T);
     return LABS_OK;
   });
   return out;
@@ -1020,9 +1100,9 @@ int labs_solver_run(labs_solver* s, int64_t epoch_iterations, double epoch_secon
   A.epoch_iters = epoch_iterations;
   A.epoch_ns = epoch_seconds >= 0 ? static_cast<int64_t>(epoch_seconds * 1e9) : -1;
   A.race = race ? 1 : 0;
-  return dispatch(s->n, [&](auto ns) -> int {
-    constexpr int NS = decltype(ns)::value;
-    return s->mt ? launch_memetic<NS, true>(ctx, A) : launch_memetic<NS, false>(ctx, A);
+  return dispatch_memetic(s->n, [&](auto ns, auto tt) -> int {
+    constexpr int NS = decltype(ns)::value, T = decltype(tt)::value;
+    return s->mt ? launch_memetic<NS, T, true>(ctx, A) : launch_memetic<NS, T, false>(ctx, A);
   });
 }
 

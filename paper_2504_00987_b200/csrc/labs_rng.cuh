@@ -1,19 +1,23 @@
-// labs_rng.cuh — warp-uniform random streams for the MTS kernels.
+// labs_rng.cuh — tile-uniform random streams for the MTS kernels.
 //
-// Every walker/replica is one warp. All 32 lanes execute each draw together
-// and obtain the same value (warp-uniform control flow), so no shuffles are
-// needed to share a draw; bulk draws (mutation) hand draw i to lane i.
+// Every walker/replica is one tile of T lanes (T = 32: a whole warp; T = 16:
+// half a warp, two replicas per warp). All lanes of a tile execute each draw
+// together and obtain the same value (tile-uniform control flow), so no
+// shuffles are needed to share a draw; bulk draws (mutation) hand draw i to
+// tile lane i. Collective operations use the tile's lane mask, so a tile may
+// draw (and refill its block) while the other tile of its warp does not.
 //
 // Two engines behind one interface:
-//  * MtRng    — reference-RNG mode. std::mt19937_64 with the state in shared
+//  * MtRngT    — reference-RNG mode. std::mt19937_64 with the state in shared
 //               memory and libstdc++ 13's distribution algorithms, restated
 //               so trajectories replay the reference bit for bit
 //               (proj/include/labsolve/rng.hpp:10-28;
 //               /usr/include/c++/13/bits/uniform_int_dist.h:255-281;
 //               /usr/include/c++/13/bits/random.tcc:3346-3381).
-//  * PhiloxRng — production mode. Counter-based Philox4x32-10 keyed by
+//  * PhiloxRngT — production mode. Counter-based Philox4x32-10 keyed by
 //               (seed, stream); draw d is half (d & 1) of block d >> 1. No
 //               per-walker state beyond a 64-bit counter.
+// Both streams are defined per draw index, independent of T.
 #pragma once
 #include <cstdint>
 
@@ -24,6 +28,56 @@ constexpr int kMtN = 312;
 constexpr int kMtM = 156;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// ------------------------------------------------------------- tiles -----
+// A tile is T consecutive lanes (T in {8, 16, 32}); tile lane = lane % T.
+template <int T>
+__device__ __forceinline__ int tile_lane() {
+  return T == 32 ? lane_id() : (lane_id() & (T - 1));
+}
+template <int T>
+__device__ __forceinline__ int tile_base() {  // warp lane of tile lane 0
+  return T == 32 ? 0 : (lane_id() & ~(T - 1));
+}
+template <int T>
+__device__ __forceinline__ unsigned tile_mask() {
+  return T == 32 ? kFull : (((1u << (T & 31)) - 1u) << tile_base<T>());
+}
+// The tile's bits of a warp-wide ballot, shifted down to bit 0.
+template <int T>
+__device__ __forceinline__ uint32_t tile_bits(uint32_t bal) {
+  return T == 32 ? bal : ((bal >> tile_base<T>()) & ((1u << (T & 31)) - 1u));
+}
+// Ballot over the tile (divergence-safe: only the tile's lanes take part).
+template <int T>
+__device__ __forceinline__ uint32_t tile_ballot(bool p) {
+  return tile_bits<T>(__ballot_sync(tile_mask<T>(), p));
+}
+template <int T>
+__device__ __forceinline__ void tile_sync() {
+  __syncwarp(tile_mask<T>());
+}
+// Divergence-safe tile reductions.
+template <int T>
+__device__ __forceinline__ int tile_sum(int v) {
+  if constexpr (T == 32) {
+    return __reduce_add_sync(kFull, v);
+  } else {
+#pragma unroll
+    for (int o = T / 2; o; o >>= 1) v += __shfl_xor_sync(tile_mask<T>(), v, o);
+    return v;
+  }
+}
+template <int T>
+__device__ __forceinline__ int tile_min(int v) {
+  if constexpr (T == 32) {
+    return __reduce_min_sync(kFull, v);
+  } else {
+#pragma unroll
+    for (int o = T / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(tile_mask<T>(), v, o));
+    return v;
+  }
+}
 
 __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
   y ^= (y >> 29) & 0x5555555555555555ULL;
@@ -66,49 +120,53 @@ __device__ __forceinline__ void sts_u64(uint32_t saddr, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(saddr), "l"(v) : "memory");
 }
 
+template <int T>
 __device__ __noinline__ void mt_twist(uint32_t mt, uint32_t out) {
-  const int lane = lane_id();
+  const int lane = tile_lane<T>();
+  const unsigned tm = tile_mask<T>();
   // i in [0, 156): inputs mt[i], mt[i+1], mt[i+156], all old.
 #pragma unroll 1
-  for (int base = 0; base < kMtN - kMtM; base += 32) {
+  for (int base = 0; base < kMtN - kMtM; base += T) {
     const uint32_t i = base + lane;
     uint64_t v = 0;
     if (i < kMtN - kMtM)
       v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)), lds_u64(mt + 8 * (i + kMtM)));
-    __syncwarp();
+    __syncwarp(tm);
     if (i < kMtN - kMtM) sts_u64(mt + 8 * i, v);
-    __syncwarp();
+    __syncwarp(tm);
   }
   // i in [156, 311): inputs mt[i], mt[i+1] old, mt[i-156] new.
 #pragma unroll 1
-  for (int base = kMtN - kMtM; base < kMtN - 1; base += 32) {
+  for (int base = kMtN - kMtM; base < kMtN - 1; base += T) {
     const uint32_t i = base + lane;
     uint64_t v = 0;
     if (i < kMtN - 1)
       v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)),
                  lds_u64(mt + 8 * (i - (kMtN - kMtM))));
-    __syncwarp();
+    __syncwarp(tm);
     if (i < kMtN - 1) sts_u64(mt + 8 * i, v);
-    __syncwarp();
+    __syncwarp(tm);
   }
   if (lane == 0)
     sts_u64(mt + 8 * (kMtN - 1),
             mt_mix(lds_u64(mt + 8 * (kMtN - 1)), lds_u64(mt), lds_u64(mt + 8 * (kMtM - 1))));
-  __syncwarp();
-  for (int i = lane; i < kMtN; i += 32) sts_u64(out + 8 * i, mt_temper(lds_u64(mt + 8 * i)));
-  __syncwarp();
+  __syncwarp(tm);
+  for (int i = lane; i < kMtN; i += T) sts_u64(out + 8 * i, mt_temper(lds_u64(mt + 8 * i)));
+  __syncwarp(tm);
 }
 
 // Temper the current block without advancing (after loading a state).
+template <int T = 32>
 __device__ __forceinline__ void mt_temper_all(const uint64_t* mt, uint64_t* out) {
-  for (int i = lane_id(); i < kMtN; i += 32) out[i] = mt_temper(mt[i]);
-  __syncwarp();
+  for (int i = tile_lane<T>(); i < kMtN; i += T) out[i] = mt_temper(mt[i]);
+  tile_sync<T>();
 }
 
-struct MtRng {
+template <int T>
+struct MtRngT {
   uint32_t mt_s;   // shared-window address of the raw engine state
   uint32_t out_s;  // shared-window address of the tempered block
-  int idx;         // warp-uniform
+  int idx;         // tile-uniform
 
   __device__ __forceinline__ void bind(uint64_t* raw, uint64_t* tempered, int i) {
     mt_s = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
@@ -117,18 +175,18 @@ struct MtRng {
   }
   __device__ __forceinline__ uint64_t next() {
     if (idx >= kMtN) {
-      mt_twist(mt_s, out_s);
+      mt_twist<T>(mt_s, out_s);
       idx = 0;
     }
     const uint64_t v = lds_u64(out_s + 8u * static_cast<uint32_t>(idx));
     ++idx;
     return v;
   }
-  // Bulk: lane i (< count) receives draw i of the next `count` draws, with
-  // count <= 32 and not crossing a twist (callers chunk on room()).
+  // Bulk: tile lane i (< count) receives draw i of the next `count` draws,
+  // with count <= T and not crossing a twist (callers chunk on room()).
   __device__ __forceinline__ int room() {
     if (idx >= kMtN) {
-      mt_twist(mt_s, out_s);
+      mt_twist<T>(mt_s, out_s);
       idx = 0;
     }
     return kMtN - idx;
@@ -138,6 +196,7 @@ struct MtRng {
   }
   __device__ __forceinline__ void advance(int count) { idx += count; }
 };
+using MtRng = MtRngT<32>;
 
 // ------------------------------------------------------------ PhiloxRng --
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0,
@@ -159,22 +218,28 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0,
   }
 }
 
-// Draws are served from a per-warp block of 64 in shared memory: a refill
-// has lane l compute Philox block (base/2 + l), i.e. draws base + 2l and
-// base + 2l + 1, so the 10-round cost is paid once per 64 draws and spread
-// over the warp. The stream is defined per draw index d (block d >> 1, half
-// d & 1), independent of the buffering.
+// Draws are served from a per-tile block of 64 in shared memory: a refill
+// has tile lane l compute Philox blocks base/2 + l + T q (q < 32/T), i.e.
+// draws base + 2(l + T q) and base + 2(l + T q) + 1, so the 10-round cost is
+// paid once per 64 draws and spread over the tile. The stream is defined per
+// draw index d (block d >> 1, half d & 1), independent of the buffering.
+template <int T>
 __device__ __noinline__ void philox_refill(uint32_t buf, uint64_t base, uint32_t k0,
                                            uint32_t k1, uint32_t s0, uint32_t s1) {
-  const uint64_t blk = (base >> 1) + static_cast<uint64_t>(lane_id());
-  uint32_t c[4] = {static_cast<uint32_t>(blk), static_cast<uint32_t>(blk >> 32), s0, s1};
-  philox4x32_10(c, k0, k1);
-  sts_u64(buf + 16u * lane_id(), static_cast<uint64_t>(c[1]) << 32 | c[0]);
-  sts_u64(buf + 16u * lane_id() + 8u, static_cast<uint64_t>(c[3]) << 32 | c[2]);
-  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 32 / T; ++q) {
+    const uint32_t rel = tile_lane<T>() + T * q;
+    const uint64_t blk = (base >> 1) + static_cast<uint64_t>(rel);
+    uint32_t c[4] = {static_cast<uint32_t>(blk), static_cast<uint32_t>(blk >> 32), s0, s1};
+    philox4x32_10(c, k0, k1);
+    sts_u64(buf + 16u * rel, static_cast<uint64_t>(c[1]) << 32 | c[0]);
+    sts_u64(buf + 16u * rel + 8u, static_cast<uint64_t>(c[3]) << 32 | c[2]);
+  }
+  tile_sync<T>();
 }
 
-struct PhiloxRng {
+template <int T>
+struct PhiloxRngT {
   static constexpr int kBlock = 64;
   uint32_t k0, k1;   // key = seed
   uint32_t s0, s1;   // stream (walker / replica id)
@@ -185,18 +250,18 @@ struct PhiloxRng {
   __device__ __forceinline__ void bind(uint64_t* buf, uint64_t c) {
     buf_s = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
     ctr = c;
-    philox_refill(buf_s, ctr & ~static_cast<uint64_t>(kBlock - 1), k0, k1, s0, s1);
+    philox_refill<T>(buf_s, ctr & ~static_cast<uint64_t>(kBlock - 1), k0, k1, s0, s1);
   }
   __device__ __forceinline__ uint64_t next() {
     const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
-    if (off == 0) philox_refill(buf_s, ctr, k0, k1, s0, s1);
+    if (off == 0) philox_refill<T>(buf_s, ctr, k0, k1, s0, s1);
     const uint64_t v = lds_u64(buf_s + 8u * off);
     ++ctr;
     return v;
   }
   __device__ __forceinline__ int room() {
     const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
-    if (off == 0) philox_refill(buf_s, ctr, k0, k1, s0, s1);
+    if (off == 0) philox_refill<T>(buf_s, ctr, k0, k1, s0, s1);
     return kBlock - static_cast<int>(off);
   }
   __device__ __forceinline__ uint64_t peek_lane(int i) const {
@@ -208,6 +273,7 @@ struct PhiloxRng {
     ctr = nc;
   }
 };
+using PhiloxRng = PhiloxRngT<32>;
 
 // ---------------------------------------------------- distributions -------
 // uniform_int_distribution<long long>(lo, hi) over a 64-bit engine: Lemire's
@@ -247,24 +313,41 @@ __device__ __forceinline__ long long uniform_int(R& rng, long long lo,
   return static_cast<long long>(static_cast<uint64_t>(lo) + __umul64hi(x, range));
 }
 
+// Rejection tail of uniform_below (taken with probability < 2^-32 per
+// draw), kept out of line so the tabu step's code stays compact (the L0
+// instruction cache is ~6 KB per SM sub-partition).
+template <class R>
+struct DrawTail {
+  uint32_t v;
+  R rng;
+};
+template <class R>
+__device__ __noinline__ DrawTail<R> uniform_below_tail(R rng, uint32_t r32, uint64_t p0,
+                                                       uint64_t p1) {
+  const uint64_t range = r32;
+  const uint64_t thr = (0ULL - range) % range;
+  uint64_t low = (p1 << 32) | static_cast<uint32_t>(p0);
+  while (low < thr) {
+    const uint64_t x = rng.next();
+    p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+    p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+    low = (p1 << 32) | static_cast<uint32_t>(p0);
+  }
+  return {static_cast<uint32_t>(p1 >> 32), rng};
+}
+
 // uniform_int(0, r - 1) for a known 32-bit range r >= 1: the same Lemire
 // arithmetic (and draw count) as uniform_int, without the range dispatch.
 template <class R>
 __device__ __forceinline__ int uniform_below(R& rng, uint32_t r32) {
-  uint64_t x = rng.next();
-  uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
-  uint64_t p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+  const uint64_t x = rng.next();
+  const uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+  const uint64_t p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
   // low 64 bits of x * r below r needs the middle word to be zero: ~2^-32.
   if (__builtin_expect(static_cast<uint32_t>(p1) == 0, 0) && static_cast<uint32_t>(p0) < r32) {
-    const uint64_t range = r32;
-    const uint64_t thr = (0ULL - range) % range;
-    uint64_t low = (p1 << 32) | static_cast<uint32_t>(p0);
-    while (low < thr) {
-      x = rng.next();
-      p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
-      p1 = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
-      low = (p1 << 32) | static_cast<uint32_t>(p0);
-    }
+    const DrawTail<R> d = uniform_below_tail(rng, r32, p0, p1);
+    rng = d.rng;
+    return static_cast<int>(d.v);
   }
   return static_cast<int>(p1 >> 32);
 }

@@ -1,7 +1,8 @@
 // labs_walker.cuh — the warp-resident LABS tabu walker (the hot path).
 //
-// One warp owns one walker. Candidate flip j lives in lane j % 32, slot
-// j / 32 (NS = ceil(n/32) slots per lane, n <= 32*NS). The reference scores
+// One tile of T lanes owns one walker (T = 32: a warp; T = 16: half a warp,
+// two walkers per warp stepping in lockstep). Candidate flip j lives in tile
+// lane j % T, slot j / T (NS slots per lane, n <= L = T*NS). The reference scores
 // every candidate with an O(n) pass over the packed product table
 // (proj/src/correlation_state.cpp:50-71), O(n^2) per tabu iteration. This
 // walker keeps four small integer vectors instead and updates all of them in
@@ -23,16 +24,20 @@
 // tests/test_oracle_cpu.py::test_incremental_identities; device parity:
 // tests/test_parity_gpu.py).
 //
-// Register layout per slot (pre-scaled so each tabu step is a few IMADs):
-//   H = 4 h_j, HQ = 4 (n - 2 + Q_{2j}), MS = -s_j, EX = expiry, CK = C_j
-//   => dE_j = HQ + MS * H (one IMAD).
-// Shared layout per warp: C mirrored as C2[L + d] = C_{|d|} so the gather
+// Register layout per slot: D = dE_j itself, MS = -s_j, EX = expiry,
+// CK = C_j. With H = 4 h_j and HQ = 4 (n - 2 + Q_{2j}), dE_j = HQ + MS H, so
+// a committed flip p changes D by
+//   j != p:  dHQ + MS dH = c16 s_{2j-p} + MS (16 s_{2p-j} + c8 (2 C_{|j-p|}
+//            + Q_{p+j})) - 32          (MS^2 = 1; c_k = -k sigma)
+//   j == p:  D -> -D                   (flipping p back undoes the move)
+// so neither h nor Q_{2j} is kept per slot.
+// Shared layout per walker: C mirrored as C2[L + d] = C_{|d|} so the gather
 // C_{|j-p|} is one LDS at a per-step base + 128 b, double-buffered (a step
 // reads one buffer and writes the other); Q[m]; spins as a zero-padded int8
 // array S[SO + x] so s_x for any x in (-L-4, 2L+4) is one LDS with the range check
 // folded into the padding. The flipped spin is stored by every lane at the
 // start of the next step (each lane then reads its own store), so a tabu
-// step needs a single warp barrier. Invalid lanes (j >= n) keep EX = INT_MAX
+// step needs a single warp barrier. Invalid positions (j >= n) keep EX = INT_MAX
 // (never admissible) and s_j = 0, which makes every update they perform a
 // no-op on the entries valid lanes read.
 #pragma once
@@ -42,14 +47,8 @@
 
 #include "labs_rng.cuh"
 
-#ifndef LABS_TIE_DUAL
-#define LABS_TIE_DUAL 0
-#endif
-#ifndef LABS_HN4
-#define LABS_HN4 0
-#endif
-#ifndef LABS_HQ_SEL
-#define LABS_HQ_SEL 0
+#ifndef LABS_TILE_BFLY
+#define LABS_TILE_BFLY 0
 #endif
 
 namespace labsk {
@@ -65,30 +64,35 @@ __device__ __forceinline__ int warp_min(int v) {
 
 __device__ __forceinline__ uint32_t lowmask(int x);
 
-template <int NS>
-struct WalkSmem {
-  static constexpr int L = 32 * NS;
+template <int L_>
+struct WalkSmemL {
+  static constexpr int L = L_;
+  static_assert(L % 32 == 0, "walker length must be a multiple of 32 positions");
+  static constexpr int NC = L / 32;  // 32-bit chunks of a sequence
   int32_t C2[2][2 * L];        // C2[buf][L + d] = C_{|d|}, d in (-L, L); 2 buffers
   int32_t Q[2 * L];            // Q[m], m in [0, 2n-1)
   static constexpr int SO = L + 4;  // spin x lives at S[SO + x]
   int8_t S[3 * L + 8];         // spins (+1/-1); 0 outside [0, n) (4 guard bytes)
-  // Packed bit windows for the O(n^2/32) popcount build, aliased onto the
-  // second C buffer (idle until the walk's first step): B32 holds s
-  // (position x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
-  static constexpr int kBitWords = 3 * NS + 2;
+  // Packed bit windows for the O(n^2/32) popcount build, aliased onto the C
+  // buffer that is idle until the walk's first step: B32 holds s (position
+  // x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
+  static constexpr int kBitWords = 3 * NC + 2;
   static_assert(2 * kBitWords <= 2 * L, "bit windows must fit one C buffer");
-  __device__ __forceinline__ uint32_t* B32() { return reinterpret_cast<uint32_t*>(C2[1]); }
-  __device__ __forceinline__ uint32_t* R32() { return B32() + kBitWords; }
-  // Zero both windows and store the payload chunks of s.
-  __device__ __forceinline__ void put_bits(int n, const uint32_t* in) {
-    uint32_t* b = B32();
-    for (int i = lane_id(); i < 2 * kBitWords; i += 32) b[i] = 0u;
-    __syncwarp();
-    if (lane_id() == 0)
-      for (int c = 0; c < NS; ++c) b[NS + c] = in[c] & lowmask(n - 32 * c);
-    __syncwarp();
+  __device__ __forceinline__ uint32_t* B32(int buf) { return reinterpret_cast<uint32_t*>(C2[buf]); }
+  __device__ __forceinline__ uint32_t* R32(int buf) { return B32(buf) + kBitWords; }
+  // Zero both windows of buffer `buf` and store the payload chunks of s.
+  template <int T>
+  __device__ __forceinline__ void put_bits(int n, const uint32_t* in, int buf) {
+    uint32_t* b = B32(buf);
+    for (int i = tile_lane<T>(); i < 2 * kBitWords; i += T) b[i] = 0u;
+    tile_sync<T>();
+    if (tile_lane<T>() == 0)
+      for (int c = 0; c < NC; ++c) b[NC + c] = in[c] & lowmask(n - 32 * c);
+    tile_sync<T>();
   }
 };
+template <int NS>
+using WalkSmem = WalkSmemL<32 * NS>;
 
 __device__ __forceinline__ uint32_t lowmask(int x) {
   return x <= 0 ? 0u : (x >= 32 ? kFull : ((1u << x) - 1u));
@@ -96,16 +100,17 @@ __device__ __forceinline__ uint32_t lowmask(int x) {
 
 // Zero the spin padding once per kernel; positions [0, n) are rewritten per
 // walk.
-template <int NS>
-__device__ __forceinline__ void smem_clear(WalkSmem<NS>& sm) {
-  for (int i = lane_id(); i < 3 * 32 * NS + 8; i += 32) sm.S[i] = 0;
-  __syncwarp();
+template <int L, int T = 32>
+__device__ __forceinline__ void smem_clear(WalkSmemL<L>& sm) {
+  for (int i = tile_lane<T>(); i < 3 * L + 8; i += T) sm.S[i] = 0;
+  tile_sync<T>();
 }
 
-// Bits [o, o+32) of a zero-padded packed array (positions [-L, 2L+32)).
-template <int NS>
+// Bits [o, o+32) of a zero-padded packed array of NC payload chunks
+// (positions [-32 NC, 64 NC + 32)).
+template <int NC>
 __device__ __forceinline__ uint32_t window32(const uint32_t* A, int o) {
-  const int u = o + 32 * NS;
+  const int u = o + 32 * NC;
   const int w = u >> 5, r = u & 31;
   return __funnelshift_r(A[w], A[w + 1], r);
 }
@@ -125,111 +130,121 @@ struct StepRec {      // mirrors labs_tabu_step (include/labs_b200.h)
   int32_t fallback;
 };
 
-template <int NS>
+template <int NS, int T = 32>
 struct Walker {
-  static constexpr int L = 32 * NS;
-  static constexpr int SO = WalkSmem<NS>::SO;
-  WalkSmem<NS>* sm;
+  static constexpr int L = T * NS;
+  using Smem = WalkSmemL<L>;
+  static constexpr int NC = Smem::NC;
+  static constexpr int SO = Smem::SO;
+  Smem* sm;
   int n;
-  int H[NS], HQ[NS], MS[NS], EX[NS], CK[NS];
+  int D[NS], MS[NS], EX[NS], CK[NS];
   int E;
   int cb;        // C2 buffer holding the current C
   int pend_pos;  // flipped position whose spin store is pending (-1: none)
   int pend_val;
 
-  // Build C, Q, h, E from `in` (chunks of 32 positions, padding zero).
-  __device__ __forceinline__ void init(int n_, const uint32_t (&in)[NS]) {
+  // Build C, Q, h, E from `in` (chunks of 32 positions, padding zero) with C
+  // in buffer cb0 (the other buffer is scratch until the first step).
+  // Divergence-safe: only the tile's lanes take part.
+  __device__ __forceinline__ void init(int n_, const uint32_t (&in)[NC], int cb0 = 0) {
     n = n_;
-    const int ln = lane_id();
-    WalkSmem<NS>& s = *sm;
+    const int ln = tile_lane<T>();
+    Smem& s = *sm;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + ln;
-      const int bit = ((in[b] & lowmask(n - 32 * b)) >> ln) & 1u;
+      const int j = T * b + ln;
+      const int c = (T * b) >> 5;
+      const int bit = ((in[c] & lowmask(n - 32 * c)) >> (((T * b) & 31) + ln)) & 1u;
       const int sp = j < n ? 1 - 2 * bit : 0;
       MS[b] = -sp;
       s.S[SO + j] = static_cast<int8_t>(sp);
       EX[b] = j < n ? 0 : INT_MAX;
     }
-    s.put_bits(n, in);
-    uint32_t* B32 = s.B32();
-    uint32_t* R32 = s.R32();
+    const int scratch = cb0 ^ 1;
+    s.template put_bits<T>(n, in, scratch);
+    uint32_t* B32 = s.B32(scratch);
+    uint32_t* R32 = s.R32(scratch);
 #pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const int i = 32 * b + ln;
-      const bool rb = i < n && s.S[SO + n - 1 - i] < 0;
-      const uint32_t m = __ballot_sync(kFull, rb);
-      if (ln == 0) R32[NS + b] = m;
+    for (int c = 0; c < NC; ++c) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = c * 32 / T; b < (c + 1) * 32 / T; ++b) {
+        const int i = T * b + ln;
+        const bool rb = i < n && s.S[SO + n - 1 - i] < 0;
+        word |= tile_ballot<T>(rb) << ((T * b) & 31);
+      }
+      if (ln == 0) R32[NC + c] = word;
     }
-    __syncwarp();
+    tile_sync<T>();
     // C_k = (n-k) - 2 popc(s xor (s >> k)) over the n-k valid pairs.
     int e2 = 0;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      const int k = 32 * b + ln;
+      const int k = T * b + ln;
       int c = 0;
       if (k >= 1 && k < n) {
         const int len = n - k;
         int acc = 0;
 #pragma unroll
-        for (int cc = 0; cc < NS; ++cc) {
-          const uint32_t a = B32[NS + cc];
-          const uint32_t x = window32<NS>(B32, 32 * cc + k);
+        for (int cc = 0; cc < NC; ++cc) {
+          const uint32_t a = B32[NC + cc];
+          const uint32_t x = window32<NC>(B32, 32 * cc + k);
           acc += __popc((a ^ x) & lowmask(len - 32 * cc));
         }
         c = len - 2 * acc;
       }
       CK[b] = c;
-      s.C2[0][L + k] = c;
-      s.C2[0][L - k] = c;
+      s.C2[cb0][L + k] = c;
+      s.C2[cb0][L - k] = c;
       e2 += c * c;
     }
-    E = __reduce_add_sync(kFull, e2);
-    cb = 0;
+    E = tile_sum<T>(e2);
+    cb = cb0;
     pend_pos = -1;
     pend_val = 0;
     // Q_m = sum_i s_i s_{m-i}: s against reversed s at offset n-1-m.
 #pragma unroll 1
     for (int a = 0; a < 2 * NS; ++a) {
-      const int m = 32 * a + ln;
+      const int m = T * a + ln;
       int qv = 0;
       if (m <= 2 * n - 2) {
         const int lo = m - n + 1 > 0 ? m - n + 1 : 0;
         const int hi = m < n - 1 ? m : n - 1;
         int acc = 0;
 #pragma unroll
-        for (int cc = 0; cc < NS; ++cc) {
+        for (int cc = 0; cc < NC; ++cc) {
           const uint32_t vm = lowmask(hi - 32 * cc + 1) & ~lowmask(lo - 32 * cc);
           if (vm) {
-            const uint32_t x = window32<NS>(R32, n - 1 - m + 32 * cc);
-            acc += __popc((B32[NS + cc] ^ x) & vm);
+            const uint32_t x = window32<NC>(R32, n - 1 - m + 32 * cc);
+            acc += __popc((B32[NC + cc] ^ x) & vm);
           }
         }
         qv = (hi - lo + 1) - 2 * acc;
       }
       s.Q[m] = qv;
     }
-    __syncwarp();
-    int h[NS];
+    tile_sync<T>();
+    int h[NS], hq[NS];
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + ln;
-      HQ[b] = 4 * (n - 2 + s.Q[2 * j]);
+      const int j = T * b + ln;
+      hq[b] = 4 * (n - 2 + s.Q[2 * j]);
       h[b] = 0;
     }
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
-    if constexpr (NS <= 4) {
-      // |C_k| <= 127: four lags per DP4A. C as int8 in the idle second C
-      // buffer (the bit windows are dead by now); spins read as 4-byte
-      // windows of S, the backward window byte-reversed.
-      int8_t* c8 = reinterpret_cast<int8_t*>(s.C2[1]);
-      for (int k = ln; k < L + 4; k += 32) c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[0][L + k] : 0);
-      __syncwarp();
+    if constexpr (L <= 128) {
+      // |C_k| <= 127: four lags per DP4A. C as int8 in the scratch C buffer
+      // (the bit windows are dead by now); spins read as 4-byte windows of
+      // S, the backward window byte-reversed.
+      int8_t* c8 = reinterpret_cast<int8_t*>(s.C2[scratch]);
+      for (int k = ln; k < L + 4; k += T) c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[cb0][L + k] : 0);
+      tile_sync<T>();
       const uint32_t* c8w = reinterpret_cast<const uint32_t*>(c8);
       const uint32_t* s32 = reinterpret_cast<const uint32_t*>(s.S);
 #pragma unroll
       for (int b = 0; b < NS; ++b) {
-        const int j = 32 * b + ln;
+        const int j = T * b + ln;
         const int fa = SO + j;          // byte of s_j (forward window start)
         const int ba = SO + j - 3;      // byte of s_{j-3} (backward window start)
         const uint32_t* fp = s32 + (fa >> 2);
@@ -245,25 +260,29 @@ struct Walker {
         }
         h[b] = acc;
       }
+      tile_sync<T>();  // c8 readers done before the scratch buffer is reused
     } else {
 #pragma unroll 2
       for (int k = 1; k < n; ++k) {
-        const int c = s.C2[0][L + k];
+        const int c = s.C2[cb0][L + k];
 #pragma unroll
         for (int b = 0; b < NS; ++b) {
-          const int j = 32 * b + ln;
+          const int j = T * b + ln;
           h[b] += c * (static_cast<int>(s.S[SO + j + k]) + static_cast<int>(s.S[SO + j - k]));
         }
       }
     }
+    // Positions j >= n (MS = 0) drift by -32 per step; starting them at
+    // 2^22 keeps them positive (never admissible, even under aspiration)
+    // for > 10^5 steps, far beyond any walk.
 #pragma unroll
-    for (int b = 0; b < NS; ++b) H[b] = 4 * h[b];
+    for (int b = 0; b < NS; ++b) D[b] = T * b + ln < n ? hq[b] + MS[b] * 4 * h[b] : (1 << 22);
   }
 
   // dE_j for every slot.
   __device__ __forceinline__ void delta(int (&dE)[NS]) const {
 #pragma unroll
-    for (int b = 0; b < NS; ++b) dE[b] = HQ[b] + MS[b] * H[b];
+    for (int b = 0; b < NS; ++b) dE[b] = D[b];
   }
 
   // Spin store of the previous flip, performed by every lane before it reads
@@ -274,27 +293,29 @@ struct Walker {
     sm->S[SO + pend_pos] = static_cast<int8_t>(pend_val);
   }
 
-  // Commit flip `pos` (warp-uniform); its expiry becomes t + tenure. Reads
+  // Commit flip `pos` (tile-uniform); its expiry becomes t + tenure. Reads
   // pre-flip values (C2[cb], Q, S) and writes C2[cb ^ 1] and Q[pos + j] (read
   // and written by lane j alone); one warp barrier orders this step's stores
-  // before the next step's loads.
+  // before the next step's loads. Called by the whole warp (converged).
   __device__ __forceinline__ void apply(int pos, int dEp, int t, int tenure) {
     if (cb) apply_cb<1>(pos, dEp, t, tenure);
     else apply_cb<0>(pos, dEp, t, tenure);
   }
 
   // apply() with the C buffer index known at compile time (the tabu loop is
-  // unrolled by two so the buffers alternate statically).
+  // unrolled by two so the buffers alternate statically); CB = -1 reads the
+  // index from `cb` (one step body, smaller code).
   template <int CB>
   __device__ __forceinline__ void apply_cb(int pos, int dEp, int t, int tenure) {
-    const int ln = lane_id();
-    WalkSmem<NS>& s = *sm;
+    const int ln = tile_lane<T>();
+    Smem& s = *sm;
     flush_spin();
     const int sig = s.S[SO + pos];
     // -2 sigma, -4 sigma, -8 sigma, -16 sigma by doubling (no multiplies)
     const int c2 = -(sig + sig), c4 = c2 + c2, c8 = c4 + c4, c16 = c8 + c8;
-    const int32_t* cgp = &s.C2[CB][L + ln - pos];
-    int32_t* cw = &s.C2[CB ^ 1][L];
+    const int cbv = CB >= 0 ? CB : cb;
+    const int32_t* cgp = &s.C2[cbv][L + ln - pos];
+    int32_t* cw = &s.C2[cbv ^ 1][L];
     int32_t* qp = &s.Q[pos + ln];
     const int8_t* s1p = &s.S[SO + 2 * pos - ln];
     const int8_t* s2p = &s.S[SO + 2 * ln - pos];
@@ -303,113 +324,172 @@ struct Walker {
     const int exp_new = t + tenure;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + ln;
+      const int j = T * b + ln;
       const bool isp = j == pos;
-      const int cg = cgp[32 * b];
-      const int qg = qp[32 * b];
-      const int s1 = s1p[-32 * b];
-      const int s2 = s2p[64 * b];
-      const int smv = smp[-32 * b];
-      const int spv = spp[32 * b];
-      // j != p: H += 16 s_{2p-j} + 32 s_j + c16 C_{|j-p|} + c8 Q_{p+j}
-#if LABS_HN4
-      const int hn = H[b] + 16 * (s1 - 2 * MS[b]) + c8 * (cg + cg + qg);
-#else
-      const int hn = H[b] + 16 * s1 - 32 * MS[b] + c8 * (cg + cg + qg);
-#endif
-      const int hp = H[b] + c2 * HQ[b];  // j == p: H -= 8 sigma (n-2+Q_2p)
-      H[b] = isp ? hp : hn;
-#if LABS_HQ_SEL
-      if (!isp) qp[32 * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
-      HQ[b] += isp ? 0 : c16 * s2;             // Q_{2j}  -= 4 sigma s_{2j-p}
-#else
-      if (!isp) {
-        qp[32 * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
-        HQ[b] += c16 * s2;             // Q_{2j}  -= 4 sigma s_{2j-p}
-      }
-#endif
+      const int cg = cgp[T * b];
+      const int qg = qp[T * b];
+      const int s1 = s1p[-T * b];
+      const int s2 = s2p[2 * T * b];
+      const int smv = smp[-T * b];
+      const int spv = spp[T * b];
+      // j != p: D += c16 s_{2j-p} + MS (16 s_{2p-j} + c8 (2 C_{|j-p|} + Q_{p+j})) - 32
+      const int wv = 16 * s1 + c8 * (cg + cg + qg);
+      const int dn = D[b] + c16 * s2 + MS[b] * wv - 32;
+      D[b] = isp ? -D[b] : dn;       // j == p: dE_p -> -dE_p
+      if (!isp) qp[T * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
       CK[b] += c2 * (smv + spv);       // C_j -= 2 sigma (s_{p-j} + s_{p+j})
       cw[j] = CK[b];
       cw[-j] = CK[b];
       MS[b] = isp ? -MS[b] : MS[b];
       EX[b] = isp ? exp_new : EX[b];
     }
-    cb = CB ^ 1;
+    cb = cbv ^ 1;
     pend_pos = pos;
     pend_val = -sig;
     E += dEp;
     __syncwarp();
   }
 
-  // Current sequence as 32-bit chunks (bit 1 = spin -1).
-  __device__ __forceinline__ void chunks(uint32_t (&out)[NS]) const {
+  // Current sequence as 32-bit chunks (bit 1 = spin -1). Divergence-safe.
+  __device__ __forceinline__ void chunks(uint32_t (&out)[NC]) const {
 #pragma unroll
-    for (int b = 0; b < NS; ++b) out[b] = __ballot_sync(kFull, MS[b] > 0);
+    for (int c = 0; c < NC; ++c) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = c * 32 / T; b < (c + 1) * 32 / T; ++b)
+        word |= tile_ballot<T>(MS[b] > 0) << ((T * b) & 31);
+      out[c] = word;
+    }
   }
 };
 
-// Value of a per-slot quantity at a warp-uniform position (one lane owns it).
-template <int NS>
+// Value of a per-slot quantity at a tile-uniform position (one lane owns it).
+template <int NS, int T = 32>
 __device__ __forceinline__ int at_position(const int (&v)[NS], int pos) {
   int mine = 0;
 #pragma unroll
-  for (int b = 0; b < NS; ++b) mine += (32 * b + lane_id() == pos) ? v[b] : 0;
-  return __reduce_add_sync(kFull, mine);
+  for (int b = 0; b < NS; ++b) mine += (T * b + tile_lane<T>() == pos) ? v[b] : 0;
+  return tile_sum<T>(mine);
 }
 
 // Position of the r-th (0-based) candidate, in ascending position order,
-// among the lanes/slots whose `hit` flag is set (msk[b] = ballot of hit[b]).
-// Rank arithmetic + a warp min keep every array index compile-time.
-template <int NS>
+// among the lanes/slots whose `hit` flag is set (msk[b] = tile ballot of
+// hit[b]). Rank arithmetic + a tile min keep every array index compile-time.
+template <int NS, int T = 32>
 __device__ __forceinline__ int nth_hit(const bool (&hit)[NS],
                                        const uint32_t (&msk)[NS], int r) {
-  const int ln = lane_id();
+  const int ln = tile_lane<T>();
   const uint32_t below = (1u << ln) - 1u;
   int base = 0, cand = INT_MAX;
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
     const int rank = base + __popc(msk[b] & below);
-    if (hit[b] && rank == r) cand = 32 * b + ln;
+    if (hit[b] && rank == r) cand = T * b + ln;
     base += __popc(msk[b]);
   }
-  return __reduce_min_sync(kFull, cand);
+  return tile_min<T>(cand);
+}
+
+// Tile minimum with the whole warp converged (the tabu step): one redux per
+// warp for T = 32; for T = 16 two reduxes over masked copies (independent,
+// so their latencies overlap); a butterfly otherwise.
+template <int T>
+__device__ __forceinline__ int tile_min_converged(int v) {
+  if constexpr (T == 32) {
+    return warp_min(v);
+  } else if constexpr (T == 16 && !LABS_TILE_BFLY) {
+    const bool hi = lane_id() >= 16;
+    const int a = warp_min(hi ? INT_MAX : v);
+    const int b = warp_min(hi ? v : INT_MAX);
+    return hi ? b : a;
+  } else {
+#pragma unroll
+    for (int o = T / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+  }
+}
+
+// Per-slot values passed by value to the out-of-line selection paths.
+template <int NS>
+struct SlotVals {
+  int v[NS];
+};
+template <class R>
+struct Pick {
+  int pos;
+  int aux;  // dE of the fallback move, or the tie count
+  R rng;
+};
+
+// Fallback of scan_neighborhood (correlation_state.cpp:156-160): nothing is
+// admissible, so one uniform_int(0, n-1) draw picks the move. Out of line:
+// rare, and it keeps the tabu step's code compact.
+template <int NS, int T, class R>
+__device__ __noinline__ Pick<R> fallback_pick(SlotVals<NS> dE, int n, R rng) {
+  const int pos = uniform_below(rng, static_cast<uint32_t>(n));
+  return {pos, at_position<NS, T>(dE.v, pos), rng};
+}
+
+// Tie among the admissible minima (correlation_state.cpp:161-165):
+// ties[uniform_int(0, #ties - 1)] in ascending position order. Out of line
+// (taken on a minority of steps).
+template <int NS, int T, class R>
+__device__ __noinline__ Pick<R> tie_pick(SlotVals<NS> key, int dmin, int pos, R rng) {
+  bool hit[NS];
+  uint32_t msk[NS];
+  int cnt = 0;
+#pragma unroll
+  for (int b = 0; b < NS; ++b) {
+    hit[b] = (key.v[b] >> 8) == dmin;
+    msk[b] = tile_ballot<T>(hit[b]);
+    cnt += __popc(msk[b]);
+  }
+  if (cnt > 1) {
+    const int r = uniform_below(rng, static_cast<uint32_t>(cnt));
+    if (r) pos = nth_hit<NS, T>(hit, msk, r);
+  }
+  return {pos, cnt, rng};
 }
 
 // Select the move at iteration t: admissible argmin with the tie/fallback
 // semantics of scan_neighborhood (proj/src/correlation_state.cpp:141-165).
-// Keys pack dE * 256 + j, so one warp min yields the minimum and its lowest
-// position (|dE| < 2^22 and j < 256 for n <= 256). A second min over the
-// other keys detects whether the minimum is tied; the tie set (ballots) is
-// only built when it is (or when FULL_TIES asks for it).
-template <int NS, bool FULL_TIES, class R>
+// Keys pack dE * 256 + j, so one tile min yields the minimum and its lowest
+// position (|dE| < 2^22 and j < 256 for n <= 256). Whether the minimum is
+// tied is decided before any tile-divergent branch (T = 32: a second min
+// over the other keys; T < 32: one warp ballot of "same dE, other position",
+// i.e. 0 < key ^ kmin < 256); the tie set (ballots) is only built when it is
+// tied (or when FULL_TIES asks for it). Must be entered by the whole warp.
+template <int NS, int T, bool FULL_TIES, class R>
 __device__ __forceinline__ void select_move(const int (&dE)[NS],
                                             const bool (&adm)[NS], int n,
                                             int tie_rule, R& rng, int& pos,
                                             int& dEp, int& fallback,
                                             uint32_t (&msk)[NS], int& ntie) {
-  const int ln = lane_id();
-  int key[NS];
+  const int ln = tile_lane<T>();
+  SlotVals<NS> key;
   int kmin = INT_MAX;
-#if LABS_TIE_DUAL
-  // Second key orders equal dE by descending position: its min is the
-  // highest tied position, reduced in parallel with the first.
-  int kmin_hi = INT_MAX;
-#endif
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
-    key[b] = adm[b] ? dE[b] * 256 + 32 * b + ln : INT_MAX;
-    kmin = min(kmin, key[b]);
-#if LABS_TIE_DUAL
-    kmin_hi = min(kmin_hi, adm[b] ? dE[b] * 256 + (255 - 32 * b - ln) : INT_MAX);
-#endif
+    key.v[b] = adm[b] ? dE[b] * 256 + T * b + ln : INT_MAX;
+    kmin = min(kmin, key.v[b]);
   }
-  kmin = warp_min(kmin);
-#if LABS_TIE_DUAL
-  if (!FULL_TIES && tie_rule == 0) kmin_hi = warp_min(kmin_hi);
-#endif
+  kmin = tile_min_converged<T>(kmin);
+  bool tied_other = false;
+  if constexpr (T < 32 && !FULL_TIES) {
+    bool h = false;
+#pragma unroll
+    for (int b = 0; b < NS; ++b)
+      h |= static_cast<uint32_t>((key.v[b] ^ kmin) - 1) < 255u;
+    tied_other = tile_bits<T>(__ballot_sync(kFull, h)) != 0u;
+  }
   if (kmin == INT_MAX) {
-    pos = uniform_below(rng, static_cast<uint32_t>(n));
-    dEp = at_position<NS>(dE, pos);
+    SlotVals<NS> d;
+#pragma unroll
+    for (int b = 0; b < NS; ++b) d.v[b] = dE[b];
+    const Pick<R> f = fallback_pick<NS, T>(d, n, rng);
+    rng = f.rng;
+    pos = f.pos;
+    dEp = f.aux;
     fallback = 1;
     ntie = 0;
 #pragma unroll
@@ -420,32 +500,38 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
   pos = kmin & 255;
   dEp = dmin;
   fallback = 0;
-  bool tied = FULL_TIES;
-  if (!FULL_TIES && tie_rule == 0) {
-#if LABS_TIE_DUAL
-    tied = (255 - (kmin_hi & 255)) != pos;
-#else
-    int k2 = INT_MAX;
-#pragma unroll
-    for (int b = 0; b < NS; ++b) k2 = min(k2, key[b] == kmin ? INT_MAX : key[b]);
-    k2 = warp_min(k2);
-    tied = (k2 >> 8) == dmin;
-#endif
-  }
   ntie = 1;
-  if (tied) {
+  if constexpr (FULL_TIES) {
+    // every tie reported (labs_scan): the tie set is always built
     bool hit[NS];
     int cnt = 0;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
-      hit[b] = (key[b] >> 8) == dmin;
-      msk[b] = __ballot_sync(kFull, hit[b]);
+      hit[b] = (key.v[b] >> 8) == dmin;
+      msk[b] = tile_ballot<T>(hit[b]);
       cnt += __popc(msk[b]);
     }
     ntie = cnt;
     if (cnt > 1 && tie_rule == 0) {
       const int r = uniform_below(rng, static_cast<uint32_t>(cnt));
-      if (r) pos = nth_hit<NS>(hit, msk, r);
+      if (r) pos = nth_hit<NS, T>(hit, msk, r);
+    }
+  } else if (tie_rule == 0) {
+    bool tied;
+    if constexpr (T < 32) {
+      tied = tied_other;
+    } else {
+      int k2 = INT_MAX;
+#pragma unroll
+      for (int b = 0; b < NS; ++b) k2 = min(k2, key.v[b] == kmin ? INT_MAX : key.v[b]);
+      k2 = warp_min(k2);
+      tied = (k2 >> 8) == dmin;
+    }
+    if (tied) {
+      const Pick<R> tp = tie_pick<NS, T>(key, dmin, pos, rng);
+      rng = tp.rng;
+      pos = tp.pos;
+      ntie = tp.aux;
     }
   }
 }
@@ -493,7 +579,7 @@ __device__ __forceinline__ int tabu_walk_impl(Walker<NS>& w, int n,
     }
     int pos, dEp, fb, ntie;
     uint32_t msk[NS];
-    select_move<NS, false>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
+    select_move<NS, 32, false>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
     const int tenure = min_t + uniform_below(rng, tenure_range);
     w.template apply_cb<decltype(cbc)::value>(pos, dEp, t, tenure);
     if (w.E < bestE) {
@@ -546,10 +632,10 @@ __device__ __forceinline__ void load_chunks(const uint64_t* w, int nw,
   }
 }
 
-template <int NS>
+template <int NS, int T = 32>
 __device__ __forceinline__ void store_chunks(uint64_t* w, int nw,
                                              const uint32_t (&c)[NS]) {
-  if (lane_id() == 0) {
+  if (tile_lane<T>() == 0) {
 #pragma unroll
     for (int wi = 0; wi < (NS + 1) / 2; ++wi) {
       if (wi < nw) {
