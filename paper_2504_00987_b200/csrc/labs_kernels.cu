@@ -331,6 +331,21 @@ __host__ __device__ constexpr int min_blocks_memetic() {
   return T * NS <= 128 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
 }
 
+// The two policy switches (aspiration, tie rule) as template parameters, so
+// the tabu step carries no runtime policy tests.
+template <int NS, int T, class R, class RB>
+__device__ __forceinline__ void run_policy(const MemeticArgs& A, Walker<NS, T>& w, R& rng,
+                                           RB& rb, TileCtl& ctl) {
+  const bool ref_ties = A.tabu.tie_rule == LABS_TIE_REFERENCE;
+  if (A.tabu.aspiration) {
+    if (ref_ties) memetic_tiles<NS, T, true, true>(A, w, rng, rb, ctl);
+    else memetic_tiles<NS, T, true, false>(A, w, rng, rb, ctl);
+  } else {
+    if (ref_ties) memetic_tiles<NS, T, false, true>(A, w, rng, rb, ctl);
+    else memetic_tiles<NS, T, false, false>(A, w, rng, rb, ctl);
+  }
+}
+
 template <int NS, int T, bool MT>
 __global__ void __launch_bounds__(32 * kWarps, (min_blocks_memetic<NS, T>()))
 k_memetic(MemeticArgs A) {
@@ -343,8 +358,7 @@ k_memetic(MemeticArgs A) {
     MtRngT<T> rng;
     rng.bind(sl.mt, sl.out, 0);  // valid until a replica is loaded
     MtBind<T> rb{A.mt, sl.mt, sl.out};
-    if (A.tabu.aspiration) memetic_tiles<NS, T, true>(A, w, rng, rb, sl.ctl);
-    else memetic_tiles<NS, T, false>(A, w, rng, rb, sl.ctl);
+    run_policy<NS, T>(A, w, rng, rb, sl.ctl);
   } else {
     PhiloxRngT<T> rng;
     rng.k0 = static_cast<uint32_t>(A.base_seed);
@@ -353,8 +367,7 @@ k_memetic(MemeticArgs A) {
     rng.s1 = 0x4D454D45u;  // "MEME"
     rng.bind(sl.out, 0);  // valid until a replica is loaded
     PhiloxBind<T> rb{A.ctr, sl.out, A.replica_offset};
-    if (A.tabu.aspiration) memetic_tiles<NS, T, true>(A, w, rng, rb, sl.ctl);
-    else memetic_tiles<NS, T, false>(A, w, rng, rb, sl.ctl);
+    run_policy<NS, T>(A, w, rng, rb, sl.ctl);
   }
 }
 

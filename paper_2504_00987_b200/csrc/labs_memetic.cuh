@@ -1,4 +1,5 @@
-// labs_memetic.cuh — the memetic layer, one warp per replica (K4).
+// labs_memetic.cuh — the memetic layer, one tile (warp or half-warp) per
+// replica (K4).
 //
 // Restates memetic_tabu (proj/src/memetic.cpp:44-117) on device: random
 // population, binary tournaments (memetic.cpp:8-22), uniform crossover
@@ -183,7 +184,7 @@ struct TileCtl {
 //
 // RB binds a replica's RNG: load(r) before its first draw, save(r) after its
 // last draw in this launch.
-template <int NS, int T, bool ASP, class R, class RB>
+template <int NS, int T, bool ASP, bool TIE_REF, class R, class RB>
 __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T>& w,
                                               R& rng, RB& rb, TileCtl& ctl) {
   constexpr int NC = (T * NS) / 32;
@@ -191,7 +192,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
   const int ln = tile_lane<T>();
   const int n = A.n, nw = A.nw, K = A.K;
   const int G = gridDim.x * (blockDim.x / T);  // tiles in the grid
-  const int tie_rule = A.tabu.tie_rule;
+  constexpr int tie_rule = TIE_REF ? 0 : 1;  // A.tabu.tie_rule, as a constant
   ctl.r = blockIdx.x * (blockDim.x / T) + static_cast<int>(threadIdx.x) / T - G;
   ctl.have = 0;
   ctl.ran = 0;

@@ -33,9 +33,9 @@
 // so neither h nor Q_{2j} is kept per slot.
 // Shared layout per walker: C mirrored as C2[L + d] = C_{|d|} so the gather
 // C_{|j-p|} is one LDS at a per-step base + 128 b, double-buffered (a step
-// reads one buffer and writes the other); Q[m]; spins as a zero-padded int8
-// array S[SO + x] so s_x for any x in (-L-4, 2L+4) is one LDS with the range check
-// folded into the padding. The flipped spin is stored by every lane at the
+// reads one buffer and writes the other); Q[m]; spins as a zero-padded array
+// S[SO + x] (int8; int32 for walkers of L <= 64) so s_x for any x in
+// (-L-4, 2L+4) is one LDS with the range check folded into the padding. The flipped spin is stored by every lane at the
 // start of the next step (each lane then reads its own store), so a tabu
 // step needs a single warp barrier. Invalid positions (j >= n) keep EX = INT_MAX
 // (never admissible) and s_j = 0, which makes every update they perform a
@@ -49,6 +49,15 @@
 
 #ifndef LABS_TILE_BFLY
 #define LABS_TILE_BFLY 0
+#endif
+#ifndef LABS_TIE_INLINE
+#define LABS_TIE_INLINE 0
+#endif
+#ifndef LABS_TIE_XOR
+#define LABS_TIE_XOR 1
+#endif
+#ifndef LABS_S4_MAX_L
+#define LABS_S4_MAX_L 64
 #endif
 
 namespace labsk {
@@ -71,8 +80,18 @@ struct WalkSmemL {
   static constexpr int NC = L / 32;  // 32-bit chunks of a sequence
   int32_t C2[2][2 * L];        // C2[buf][L + d] = C_{|d|}, d in (-L, L); 2 buffers
   int32_t Q[2 * L];            // Q[m], m in [0, 2n-1)
-  static constexpr int SO = L + 4;  // spin x lives at S[SO + x]
+  static constexpr int SO = L + 4;  // spin x lives at S[SO + x] and S4[SO + x]
   int8_t S[3 * L + 8];         // spins (+1/-1); 0 outside [0, n) (4 guard bytes)
+  // For L <= LABS_S4_MAX_L the tabu step keeps its spins in an int32 copy
+  // instead (its gathers then share scaled index registers with the Q
+  // gather: +3% at n = 64, B200); for longer walkers the extra shared memory
+  // costs more than it saves (-3% at n = 119), so the step uses S itself.
+  static constexpr bool kS4 = L <= LABS_S4_MAX_L;
+  int32_t S4[kS4 ? 3 * L + 8 : 1];
+  __device__ __forceinline__ auto* spins() {
+    if constexpr (kS4) return S4;
+    else return S;
+  }
   // Packed bit windows for the O(n^2/32) popcount build, aliased onto the C
   // buffer that is idle until the walk's first step: B32 holds s (position
   // x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
@@ -102,7 +121,10 @@ __device__ __forceinline__ uint32_t lowmask(int x) {
 // walk.
 template <int L, int T = 32>
 __device__ __forceinline__ void smem_clear(WalkSmemL<L>& sm) {
-  for (int i = tile_lane<T>(); i < 3 * L + 8; i += T) sm.S[i] = 0;
+  for (int i = tile_lane<T>(); i < 3 * L + 8; i += T) {
+    sm.S[i] = 0;
+    if constexpr (WalkSmemL<L>::kS4) sm.S4[i] = 0;
+  }
   tile_sync<T>();
 }
 
@@ -159,6 +181,7 @@ struct Walker {
       const int sp = j < n ? 1 - 2 * bit : 0;
       MS[b] = -sp;
       s.S[SO + j] = static_cast<int8_t>(sp);
+      if constexpr (Smem::kS4) s.S4[SO + j] = sp;
       EX[b] = j < n ? 0 : INT_MAX;
     }
     const int scratch = cb0 ^ 1;
@@ -290,7 +313,8 @@ struct Walker {
   // (pend_pos = -1, pend_val = 0 after init rewrites the zero padding byte
   // of position -1, so the store needs no guard.)
   __device__ __forceinline__ void flush_spin() {
-    sm->S[SO + pend_pos] = static_cast<int8_t>(pend_val);
+    using E = std::remove_pointer_t<decltype(sm->spins())>;
+    sm->spins()[SO + pend_pos] = static_cast<E>(pend_val);
   }
 
   // Commit flip `pos` (tile-uniform); its expiry becomes t + tenure. Reads
@@ -310,17 +334,18 @@ struct Walker {
     const int ln = tile_lane<T>();
     Smem& s = *sm;
     flush_spin();
-    const int sig = s.S[SO + pos];
+    const auto* sp0 = s.spins();  // int32 (short walkers) or int8 spins
+    const int sig = sp0[SO + pos];
     // -2 sigma, -4 sigma, -8 sigma, -16 sigma by doubling (no multiplies)
     const int c2 = -(sig + sig), c4 = c2 + c2, c8 = c4 + c4, c16 = c8 + c8;
     const int cbv = CB >= 0 ? CB : cb;
     const int32_t* cgp = &s.C2[cbv][L + ln - pos];
     int32_t* cw = &s.C2[cbv ^ 1][L];
     int32_t* qp = &s.Q[pos + ln];
-    const int8_t* s1p = &s.S[SO + 2 * pos - ln];
-    const int8_t* s2p = &s.S[SO + 2 * ln - pos];
-    const int8_t* smp = &s.S[SO + pos - ln];
-    const int8_t* spp = &s.S[SO + pos + ln];
+    const auto* s1p = &sp0[SO + 2 * pos - ln];
+    const auto* s2p = &sp0[SO + 2 * ln - pos];
+    const auto* smp = &sp0[SO + pos - ln];
+    const auto* spp = &sp0[SO + pos + ln];
     const int exp_new = t + tenure;
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
@@ -475,7 +500,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
   }
   kmin = tile_min_converged<T>(kmin);
   bool tied_other = false;
-  if constexpr (T < 32 && !FULL_TIES) {
+  if constexpr ((T < 32 || LABS_TIE_XOR) && !FULL_TIES) {
     bool h = false;
 #pragma unroll
     for (int b = 0; b < NS; ++b)
@@ -518,7 +543,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
     }
   } else if (tie_rule == 0) {
     bool tied;
-    if constexpr (T < 32) {
+    if constexpr (T < 32 || LABS_TIE_XOR) {
       tied = tied_other;
     } else {
       int k2 = INT_MAX;
@@ -528,10 +553,26 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
       tied = (k2 >> 8) == dmin;
     }
     if (tied) {
-      const Pick<R> tp = tie_pick<NS, T>(key, dmin, pos, rng);
-      rng = tp.rng;
-      pos = tp.pos;
-      ntie = tp.aux;
+      if constexpr (LABS_TIE_INLINE) {
+        bool hit[NS];
+        int cnt = 0;
+#pragma unroll
+        for (int b = 0; b < NS; ++b) {
+          hit[b] = (key.v[b] >> 8) == dmin;
+          msk[b] = tile_ballot<T>(hit[b]);
+          cnt += __popc(msk[b]);
+        }
+        ntie = cnt;
+        if (cnt > 1) {
+          const int r = uniform_below(rng, static_cast<uint32_t>(cnt));
+          if (r) pos = nth_hit<NS, T>(hit, msk, r);
+        }
+      } else {
+        const Pick<R> tp = tie_pick<NS, T>(key, dmin, pos, rng);
+        rng = tp.rng;
+        pos = tp.pos;
+        ntie = tp.aux;
+      }
     }
   }
 }

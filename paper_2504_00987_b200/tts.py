@@ -122,14 +122,17 @@ def fit_exponential(samples, n_min, n_max):
             "n_min_fit": n_min, "n_max_fit": n_max, "points_used": m}
 
 
-def read_targets(path):
+def read_targets(path, column=1):
+    """n -> target energy from whitespace columns (n, E, ...); `column`
+    picks which energy column (targets_long.txt: 1 = the paper's record,
+    2 = the previous literature best)."""
     t = {}
     with open(path) as f:
         for line in f:
             line = line.strip()
             if line and not line.startswith("#"):
-                n, e = line.split()[:2]
-                t[int(n)] = int(e)
+                cols = line.split()
+                t[int(cols[0])] = int(cols[column])
     return t
 
 
@@ -178,6 +181,8 @@ def main(argv=None):
     ap.add_argument("--time-limit", type=float, default=60.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--fit", default=None, help="n_min-n_max window")
+    ap.add_argument("--target-column", type=int, default=1,
+                    help="energy column of --targets (targets_long.txt: 2 = previous best)")
     args = ap.parse_args(argv)
     if "-" in args.n:
         a, b = map(int, args.n.split("-"))
@@ -186,7 +191,7 @@ def main(argv=None):
         ns = [int(x) for x in args.n.split(",")]
     from paper_2504_00987_b200 import capi
     ctx = capi.Context(0)
-    targets = read_targets(args.targets)
+    targets = read_targets(args.targets, args.target_column)
     fh = open(args.out, "a") if args.out else None
 
     def log(rec):

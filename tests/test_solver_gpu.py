@@ -171,3 +171,23 @@ def test_more_replicas_than_resident_warps(ctx, oracle):
         assert per[r]["best"].tolist() == want["best"]
         assert per[r]["best_energy"] == want["best_energy"]
     assert best["best_energy"] == min(x["best_energy"] for x in per)
+
+
+@pytest.mark.parametrize("kind", [capi.RNG_PHILOX, capi.RNG_MT19937_64])
+@pytest.mark.parametrize("n,asp,tie", [(30, 0, capi.TIE_REFERENCE), (64, 1, capi.TIE_LOWEST),
+                                       (50, 0, capi.TIE_REFERENCE)])
+def test_tile_widths_agree(ctx, monkeypatch, kind, n, asp, tie):
+    """K4 with two replicas per warp (16-lane tiles) and with one per warp
+    runs every replica through the same trajectory: both RNG streams are
+    defined per draw, independent of the tile width. Odd replica counts leave
+    a half-idle warp at the end of the grid."""
+    p = capi.memetic_params(target_energy=0, max_iterations=4, rng_kind=kind,
+                            tie_rule=tie, aspiration=bool(asp))
+    out = {}
+    for tile in ("32", "16"):
+        monkeypatch.setenv("LABS_TILE", tile)
+        sv = capi.Solver(ctx, n, 37, base_seed=11, params=p)
+        sv.run(race=False)
+        out[tile] = (_results(sv), sv.population()[1].tolist())
+        sv.close()
+    assert out["16"] == out["32"]

@@ -7,5 +7,6 @@ LABS_TILE=$t timeout 300 ncu --set full --clock-control none --import-source on 
 tail -1 gpurun_out/ncu_t$t.log
 ncu -i /tmp/prof_t$t.ncu-rep --page raw --csv > gpurun_out/prof_t${t}_raw.csv 2>&1
 ncu -i /tmp/prof_t$t.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_t${t}_sass.csv 2>&1
+ncu -i /tmp/prof_t$t.ncu-rep --page source --csv --print-source cuda > gpurun_out/prof_t${t}_cuda.csv 2>&1
 ls -la gpurun_out/prof_t${t}_*.csv
 done
