@@ -318,3 +318,19 @@ def test_solve_cli_wire_format(tmp_path):
     bad = subprocess.run([sys.executable, "-m", "paper_2504_00987_b200.solve", "--n", "1"],
                          capture_output=True, text=True, timeout=120)
     assert bad.returncode == 2
+
+
+@pytest.mark.parametrize("n,lo,hi,iters", [(60, 0.10, 0.90, 6), (200, 0.0, 0.95, 2),
+                                           (33, 0.0, 0.0, 8)])
+def test_memetic_wide_tenure_windows(ctx, oracle, n, lo, hi, iters):
+    """Tenure windows far from the default 0.10/0.12 (wide ones exercise the
+    range-specialized Lemire reduction with large ranges; a one-value window
+    still consumes one draw per step). Whole memetic runs must replay the
+    oracle draw for draw."""
+    kw = dict(min_tabu_factor=lo, max_tabu_factor=hi)
+    want = oracle.memetic(n, 4242, child_cap=iters, max_iterations=iters, **kw)
+    d = ctx.memetic(n, 4242, capi.memetic_params(max_iterations=iters, **kw), trace_cap=iters + 1)
+    assert d["best_energy"] == want["best_energy"]
+    assert d["best"].tolist() == want["best"]
+    assert d["iterations"] == want["iterations"]
+    assert [t[2] for t in d["trace"]] == want["child_energies"]
