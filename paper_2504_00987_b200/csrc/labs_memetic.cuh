@@ -442,6 +442,13 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
     ++t;
   };
 
+  // Has any tile's walk ended? With one tile per warp t and m are
+  // warp-uniform, so no vote is needed.
+  auto walk_ended = [&]() -> bool {
+    if constexpr (T == 32) return t > m;
+    else return __any_sync(kFull, t > m);
+  };
+
   // Outer loop: bookkeeping for the tiles whose walk ended. Inner loop (the
   // hot one): steps until some tile's walk ends. Unrolled by two (the C
   // buffers alternate statically) when both step bodies fit the L0
@@ -453,13 +460,13 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
       if (par) goto odd;
       while (true) {
         step(std::integral_constant<int, 0>{});
-        if (__any_sync(kFull, t > m)) {
+        if (walk_ended()) {
           par = 1;
           break;
         }
       odd:
         step(std::integral_constant<int, 1>{});
-        if (__any_sync(kFull, t > m)) {
+        if (walk_ended()) {
           par = 0;
           break;
         }
@@ -467,7 +474,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
     } else {
       do {
         step(std::integral_constant<int, -1>{});
-      } while (!__any_sync(kFull, t > m));
+      } while (!walk_ended());
     }
   }
 }

@@ -505,7 +505,8 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
 #pragma unroll
     for (int b = 0; b < NS; ++b)
       h |= static_cast<uint32_t>((key.v[b] ^ kmin) - 1) < 255u;
-    tied_other = tile_bits<T>(__ballot_sync(kFull, h)) != 0u;
+    if constexpr (T == 32) tied_other = __any_sync(kFull, h);
+    else tied_other = tile_bits<T>(__ballot_sync(kFull, h)) != 0u;
   }
   if (kmin == INT_MAX) {
     SlotVals<NS> d;
