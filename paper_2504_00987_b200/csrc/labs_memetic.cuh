@@ -75,6 +75,18 @@ __device__ __forceinline__ int64_t globaltimer_ns() {
   return static_cast<int64_t>(t);
 }
 
+// Tile-uniform reads of values other agents change concurrently (the global
+// timer, the stop flag): tile lane 0 reads, the tile agrees, so every lane
+// takes the same branch.
+template <int T>
+__device__ __forceinline__ int64_t tile_globaltimer_ns() {
+  return __shfl_sync(tile_mask<T>(), globaltimer_ns(), 0, T);
+}
+template <int T>
+__device__ __forceinline__ bool tile_stop_seen(const volatile int32_t* stop) {
+  return __shfl_sync(tile_mask<T>(), *stop, 0, T) != 0;
+}
+
 // E = sum C_k^2 of a sequence given as chunks (uses scratch C buffer 1's
 // bit windows; only called while the tile has no walk in flight).
 template <int NS, int T>
@@ -160,7 +172,9 @@ __device__ __forceinline__ int tournament(const int32_t* e, int K, R& rng) {
 
 // Cold per-tile replica bookkeeping, kept in shared memory so that it does
 // not occupy registers across the tabu loop. Every lane of the tile reads
-// and writes identical values (same-value stores need no ordering).
+// and writes identical values; an update reads its operands, waits at a
+// tile barrier, then writes, so no lane can overwrite a value another lane
+// has yet to read.
 struct TileCtl {
   int64_t it, it_start, t0, tlen, resume_ns;
   unsigned long long tabu_steps;
@@ -207,11 +221,15 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
   // Finish the walk that just ended (memetic.cpp:94-107).
   auto post_walk = [&]() {
     const int r = ctl.r;
+    const unsigned long long steps0 = ctl.tabu_steps;
+    const int best0 = ctl.bestE;
+    const int64_t tlen0 = ctl.tlen, it0 = ctl.it;
+    tile_sync<T>();
     uint64_t* pop = A.pop + static_cast<size_t>(r) * K * nw;
     int32_t* popE = A.popE + static_cast<size_t>(r) * K;
-    ctl.tabu_steps += static_cast<unsigned long long>(m);
+    ctl.tabu_steps = steps0 + static_cast<unsigned long long>(m);
     const int re = wbestE;
-    if (re < ctl.bestE) {
+    if (re < best0) {
       ctl.bestE = re;
       store_chunks<NC, T>(A.best + static_cast<size_t>(r) * nw, nw, wbest);
     }
@@ -228,16 +246,16 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
         if (ln == 0) popE[victim] = re;
       }
     }
-    if (A.trace && ctl.tlen < A.trace_cap && ln == 0) {
-      int64_t* rec = A.trace + (static_cast<size_t>(r) * A.trace_cap + ctl.tlen) * 3;
-      rec[0] = ctl.it;
+    if (A.trace && tlen0 < A.trace_cap && ln == 0) {
+      int64_t* rec = A.trace + (static_cast<size_t>(r) * A.trace_cap + tlen0) * 3;
+      rec[0] = it0;
       rec[1] = 0;
       rec[2] = re;
     }
-    ctl.tlen = ctl.tlen + 1;
-    ctl.it = ctl.it + 1;
+    ctl.tlen = tlen0 + 1;
+    ctl.it = it0 + 1;
     tile_sync<T>();
-    if (A.race && !(static_cast<int64_t>(ctl.bestE) > A.target) && ln == 0)
+    if (A.race && !(static_cast<int64_t>(re < best0 ? re : best0) > A.target) && ln == 0)
       *A.stop = 1;  // parallel.cpp:40 — reaching the target raises the flag
   };
 
@@ -266,6 +284,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
   auto next_replica = [&]() -> bool {
     while (true) {
       const int r = ctl.r + G;
+      tile_sync<T>();
       if (r >= A.replicas) return false;
       ctl.r = r;
       if (A.initialized[r] && A.status[r] != kRunning) continue;
@@ -301,7 +320,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
           A.iters[r] = 0;
           A.status[r] = kRunning;
           A.initialized[r] = 1;
-          A.t0[r] = globaltimer_ns();
+          A.t0[r] = globaltimer_ns();  // lane 0 only
           if (A.trace_len) A.trace_len[r] = 0;
         }
         tile_sync<T>();
@@ -311,7 +330,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
       ctl.it_start = ctl.it;
       ctl.t0 = A.t0[r];
       ctl.tlen = A.trace_len ? A.trace_len[r] : 0;
-      ctl.resume_ns = globaltimer_ns();
+      ctl.resume_ns = tile_globaltimer_ns<T>();
       ctl.tabu_steps = 0;
       ctl.have = 1;
       return true;
@@ -340,21 +359,23 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
       int32_t st = -1;
       if (!(static_cast<int64_t>(ctl.bestE) > A.target)) {
         st = kReached;
-      } else if (*A.stop) {
-        if (A.trace && ctl.tlen < A.trace_cap && ln == 0) {
-          int64_t* rec = A.trace + (static_cast<size_t>(r) * A.trace_cap + ctl.tlen) * 3;
+      } else if (tile_stop_seen<T>(A.stop)) {
+        const int64_t tlen0 = ctl.tlen;
+        tile_sync<T>();
+        if (A.trace && tlen0 < A.trace_cap && ln == 0) {
+          int64_t* rec = A.trace + (static_cast<size_t>(r) * A.trace_cap + tlen0) * 3;
           rec[0] = ctl.it;
           rec[1] = 1;
           rec[2] = -1;
         }
-        ctl.tlen = ctl.tlen + 1;
+        ctl.tlen = tlen0 + 1;
         st = kStopped;
       } else if (A.max_iterations >= 0 && ctl.it >= A.max_iterations) {
         st = kMaxIter;
-      } else if (A.max_ns >= 0 && globaltimer_ns() - ctl.t0 >= A.max_ns) {
+      } else if (A.max_ns >= 0 && tile_globaltimer_ns<T>() - ctl.t0 >= A.max_ns) {
         st = kTimeout;
       } else if ((A.epoch_iters >= 0 && ctl.it - ctl.it_start >= A.epoch_iters) ||
-                 (A.epoch_ns >= 0 && globaltimer_ns() - ctl.resume_ns >= A.epoch_ns)) {
+                 (A.epoch_ns >= 0 && tile_globaltimer_ns<T>() - ctl.resume_ns >= A.epoch_ns)) {
         st = kRunning;  // epoch over: the replica continues in the next launch
       }
       if (st >= 0) {

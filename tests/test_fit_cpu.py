@@ -44,3 +44,16 @@ def test_python_fit_matches_reference_semantics():
               "reachedTarget": True} for n in range(10, 31)]
     f = tts.fit_exponential(noisy, 10, 30)
     assert f["b_ci"][0] < 1.25 < f["b_ci"][1]
+
+
+def test_read_targets_columns():
+    """targets_long.txt: column 1 = the paper's records (= the reference's
+    proj/data/targets_published.txt), column 2 = the previous best-known."""
+    import os
+    from paper_2504_00987_b200 import tts
+    path = os.path.join(os.path.dirname(tts.__file__), "data", "targets_long.txt")
+    new, old = tts.read_targets(path), tts.read_targets(path, 2)
+    assert new[92] == 490 and old[92] == 498
+    assert new[119] == 787 and old[119] == 835
+    assert set(new) == set(old) and len(new) == 16
+    assert all(new[n] <= old[n] for n in new)
