@@ -78,13 +78,21 @@ __device__ __forceinline__ int64_t globaltimer_ns() {
 // Tile-uniform reads of values other agents change concurrently (the global
 // timer, the stop flag): tile lane 0 reads, the tile agrees, so every lane
 // takes the same branch.
+#ifndef LABS_BCAST_READS
+#define LABS_BCAST_READS 1
+#endif
+#ifndef LABS_CTL_SYNC
+#define LABS_CTL_SYNC 1
+#endif
 template <int T>
 __device__ __forceinline__ int64_t tile_globaltimer_ns() {
-  return __shfl_sync(tile_mask<T>(), globaltimer_ns(), 0, T);
+  if constexpr (LABS_BCAST_READS) return __shfl_sync(tile_mask<T>(), globaltimer_ns(), 0, T);
+  else return globaltimer_ns();
 }
 template <int T>
 __device__ __forceinline__ bool tile_stop_seen(const volatile int32_t* stop) {
-  return __shfl_sync(tile_mask<T>(), *stop, 0, T) != 0;
+  if constexpr (LABS_BCAST_READS) return __shfl_sync(tile_mask<T>(), *stop, 0, T) != 0;
+  else return *stop != 0;
 }
 
 // E = sum C_k^2 of a sequence given as chunks (uses scratch C buffer 1's
@@ -224,7 +232,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
     const unsigned long long steps0 = ctl.tabu_steps;
     const int best0 = ctl.bestE;
     const int64_t tlen0 = ctl.tlen, it0 = ctl.it;
-    tile_sync<T>();
+    if constexpr (LABS_CTL_SYNC) tile_sync<T>();
     uint64_t* pop = A.pop + static_cast<size_t>(r) * K * nw;
     int32_t* popE = A.popE + static_cast<size_t>(r) * K;
     ctl.tabu_steps = steps0 + static_cast<unsigned long long>(m);
@@ -284,7 +292,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
   auto next_replica = [&]() -> bool {
     while (true) {
       const int r = ctl.r + G;
-      tile_sync<T>();
+      if constexpr (LABS_CTL_SYNC) tile_sync<T>();
       if (r >= A.replicas) return false;
       ctl.r = r;
       if (A.initialized[r] && A.status[r] != kRunning) continue;
@@ -361,7 +369,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
         st = kReached;
       } else if (tile_stop_seen<T>(A.stop)) {
         const int64_t tlen0 = ctl.tlen;
-        tile_sync<T>();
+        if constexpr (LABS_CTL_SYNC) tile_sync<T>();
         if (A.trace && tlen0 < A.trace_cap && ln == 0) {
           int64_t* rec = A.trace + (static_cast<size_t>(r) * A.trace_cap + tlen0) * 3;
           rec[0] = ctl.it;
