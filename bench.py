@@ -17,13 +17,19 @@ iteration).
           population init and result copy-back inside the timed region).
   cpu_baseline   the reference's own tabu_search (oracle/_ref, unmodified
           sources) on every host core for --cpu-seconds.
-  tts     time to the best-known energy (N=64 -> 208) on this GPU.
+  tts     time to the best-known energy (N=64 -> 208) on this GPU: >= 10
+          samples from disjoint seed blocks base + run * R (fit.cpp:30-31),
+          median / Q1 / Q3 / censored count, the winning sequence per sample;
+          cpu_tts: the reference's own run_replicas (oracle/_ref) on every
+          host core racing to the same target, censored at a stated limit.
 
 --impl reference runs the reference's multithreaded CPU tabu_search on the
 host cores with the same metric (rank 0 only under torchrun).
-Multi-GPU (torchrun, one rank per GPU): each rank runs its own replica set
-(global replica ids rank*R + r, seeds base + id); weak scaling, no data-path
-collective. The island model (elite allgather) is exercised by --islands.
+Multi-GPU: `--gpus N` (N > 1) re-executes itself under torch.distributed.run
+with N ranks (one per GPU) unless it already runs under torchrun; each rank
+runs its own replica set (global replica ids rank*R + r, seeds base + id);
+weak scaling, no data-path collective. The island model (elite allgather) is
+exercised by --islands.
 """
 from __future__ import annotations
 
@@ -42,6 +48,7 @@ sys.path.insert(0, ROOT)
 
 OPS_PER_FLIP_EVAL = 13  # int32 ops per candidate per tabu iteration
 TARGETS = {32: 64, 64: 208}  # Packebusch & Mertens 2016 optima
+PAPER_A100_FIT = (8.23e-8, 1.313)  # TTS(N) = a * b^N s
 
 
 def parse():
@@ -55,8 +62,11 @@ def parse():
     ap.add_argument("--rng", choices=["mt19937_64", "philox"], default="mt19937_64")
     ap.add_argument("--replicas", type=int, default=0, help="0 = resident capacity")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--tts-seeds", type=int, default=3)
-    ap.add_argument("--tts-limit", type=float, default=30.0)
+    ap.add_argument("--tts-samples", type=int, default=12,
+                    help="disjoint-seed TTS samples at N=64 (0 = skip)")
+    ap.add_argument("--tts-limit", type=float, default=20.0)
+    ap.add_argument("--cpu-tts-seconds", type=float, default=20.0,
+                    help="censoring limit of the reference CPU run_replicas TTS")
     ap.add_argument("--islands", type=int, default=0,
                     help="elite exchange every this many steps (0 = off)")
     ap.add_argument("--quick", action="store_true", help="skip cpu baseline and TTS")
@@ -114,6 +124,61 @@ def dist_setup():
     return world, rank, local
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """`--gpus N` outside torchrun: re-exec under torch.distributed.run with
+    N ranks, after checking that N devices are visible (fail loudly)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices; "
+                             f"{have} visible\n")
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stderr.write("bench.py: launching " + " ".join(cmd[1:6]) + "\n")
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def admissible_fraction(n: int, walks: int = 200) -> float:
+    """Mean fraction of the N candidates that are admissible (not tabu) per
+    tabu iteration — the share the reference actually scores
+    (tabu.cpp:43-44) — from oracle walks of random starts."""
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    adm, tot = 0, 0
+    for w in range(walks):
+        start = o.random_sequence(n, o.rng(7000 + w))
+        out = o.tabu(n, start, o.rng(9000 + w), trace=True)
+        expiry = [0] * n
+        for (t, pos, _e, tenure, _fb) in out["steps"]:
+            adm += sum(1 for j in range(n) if expiry[j] < t)
+            tot += n
+            expiry[pos] = t + tenure
+    return adm / tot
+
+
 def cpu_reference_throughput(n: int, seconds: float):
     """The reference's tabu_search on every host core (or the oracle port)."""
     from oracle.pyoracle import Oracle, Reference, reference_available
@@ -125,8 +190,28 @@ def cpu_reference_throughput(n: int, seconds: float):
         it, walks, el = Oracle().tabu_throughput(n, threads, seconds)
         kind = "port"
     return {"value": it * n / el, "unit": "flip-evals/s", "cores": threads, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"{walks} tabu_search walks from Sequence::random({n}), "
                       f"{threads} threads x {seconds:.0f} s, TabuParams{{0.10,0.12}}"}
+
+
+def cpu_reference_tts(n: int, target: int, seconds: float, base_seed: int = 50_000):
+    """The reference's own run_replicas (oracle/_ref, threaded, replicas =
+    host cores) racing to `target`, censored at `seconds` (run_tts,
+    fit.cpp:15-41)."""
+    from oracle.pyoracle import Reference, reference_available
+    threads = os.cpu_count() or 1
+    if not reference_available():
+        return {"unavailable": "oracle/_ref not built"}
+    t0 = time.perf_counter()
+    best, _ = Reference().run_replicas(n, threads, base_seed, threaded=True,
+                                       target_energy=target, max_seconds=seconds)
+    dt = time.perf_counter() - t0
+    reached = best["best_energy"] <= target
+    return {"n": n, "target": target, "replicas": threads, "cores": threads,
+            "cpu_model": cpu_model(), "limit_s": seconds, "runtime_s": dt,
+            "reachedTarget": reached, "censored": not reached,
+            "bestE": best["best_energy"], "seed": base_seed, "kind": "reference"}
 
 
 def run_reference(args, world, rank):
@@ -158,7 +243,11 @@ def run_reference(args, world, rank):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     world, rank, local = dist_setup()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.stderr.write(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
@@ -166,9 +255,16 @@ def main():
     import torch.distributed as dist
     from paper_2504_00987_b200 import capi
 
+    if torch.cuda.device_count() <= local:
+        sys.stderr.write(f"bench.py: rank {rank} needs cuda:{local}; "
+                         f"{torch.cuda.device_count()} device(s) visible\n")
+        sys.exit(2)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+        sys.stderr.write(f"bench.py: rank {rank}/{world} on cuda:{local}, NCCL communicator "
+                         f"up (backend {dist.get_backend()})\n")
     ctx = capi.Context(local)
     ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     n = args.n
@@ -228,12 +324,15 @@ def main():
     value = evals_total / (time_ms / 1e3)
     per_gpu = value / world
 
-    # roofline: the memetic kernel is the step (one launch per step)
-    peak_gops = ctx.int_peak_gops()
-    achieved_gops = per_gpu * OPS_PER_FLIP_EVAL / 1e9
-    # DRAM bytes per launch from the committed ncu capture, scaled to this
-    # run's epoch length (the kernel's traffic is per memetic iteration).
-    traffic, issue = None, None
+    # Roofline: (N-1) lag-term MACs per flip-evaluation over
+    # the measured IMAD rate of this device. The kernel's O(1)-per-candidate
+    # update does far fewer operations than the reference's O(N) scoring, so
+    # frac > 1 is possible; executed_* keys give the work actually issued.
+    imad_peak = ctx.imad_peak_gops()
+    int_peak = ctx.int_peak_gops()
+    lag_gmacs = per_gpu * (n - 1) / 1e9
+    exec_gops = per_gpu * OPS_PER_FLIP_EVAL / 1e9
+    traffic, issue, prof_src = None, None, None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
@@ -241,6 +340,7 @@ def main():
             per_ms = pj.get(f"k_memetic_n{n}_dram_bytes_per_ms")
             traffic = per_ms * (time_ms / args.steps) if per_ms else None
             issue = pj.get(f"k_memetic_n{n}_issue_slots_busy")
+            prof_src = pj.get("source")
         except Exception:
             traffic = None
 
@@ -252,6 +352,8 @@ def main():
                                      rng_kind=rng_kind)
     ctx.run_replicas(n, R, 7, capi.memetic_params(target_energy=0, max_iterations=2,
                                                   rng_kind=rng_kind))  # warm
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     best, per = ctx.run_replicas(n, R, 1000 + rank * R, e2e_params)
     e2e_t = time.perf_counter() - t0
@@ -282,11 +384,18 @@ def main():
         "per_gpu": per_gpu,
         "memetic_iterations": m_after - m_before,
         "gpu_launches": launches,
-        "roofline": {"bound": "int32", "achieved": achieved_gops, "peak": peak_gops,
-                     "unit": "Gop/s", "frac": achieved_gops / peak_gops, "traffic": traffic,
-                     "ops_per_flip_eval": OPS_PER_FLIP_EVAL,
-                     "peak_source": "measured on this device (labs_bench_int_peak)",
-                     "lag_term_equiv_frac": per_gpu * (n - 1) / (peak_gops * 1e9),
+        "roofline": {"bound": "int32", "achieved": lag_gmacs, "peak": imad_peak,
+                     "unit": "Gop/s", "frac": lag_gmacs / imad_peak, "traffic": traffic,
+                     "traffic_source": (f"extrapolated_from_ncu ({prof_src}): DRAM bytes per "
+                                        "ms of k_memetic x this run's launch length")
+                     if traffic is not None else None,
+                     "work_per_flip_eval": f"{n - 1} lag-term MACs (N-1, SURVEY.md §8d)",
+                     "peak_source": "IMAD-only probe labs_bench_imad_peak, measured on "
+                                    "this device in this run",
+                     "frac_vs_all_int_pipes": lag_gmacs / int_peak,
+                     "int_peak_all_pipes": int_peak,
+                     "executed_ops_per_flip_eval": OPS_PER_FLIP_EVAL,
+                     "executed_ops_frac": exec_gops / int_peak,
                      "issue_slots_busy_ncu": issue},
         "e2e": {"value": e2e_value, "unit": "flip-evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
@@ -297,37 +406,44 @@ def main():
 
     if rank == 0 and world == 1 and not args.quick:
         try:
-            line["cpu_baseline"] = cpu_reference_throughput(n, args.cpu_seconds)
+            cb = cpu_reference_throughput(n, args.cpu_seconds)
+            frac = admissible_fraction(n)
+            cb["admissible_fraction"] = frac
+            cb["value_admissible_only"] = cb["value"] * frac
+            line["cpu_baseline"] = cb
         except Exception as e:  # the checker library was not built on this host
             line["cpu_baseline"] = {"unavailable": f"{type(e).__name__}: {e}"}
-        if n in TARGETS and args.tts_seeds > 0:
-            line["tts"] = time_to_target(ctx, capi, n, TARGETS[n], R, rng_kind, args)
+        if n in TARGETS and args.tts_samples > 0:
+            line["tts"] = time_to_target(ctx, n, TARGETS[n], R, rng_kind, args)
+            try:
+                line["tts"]["cpu_tts"] = cpu_reference_tts(n, TARGETS[n], args.cpu_tts_seconds)
+            except Exception as e:
+                line["tts"]["cpu_tts"] = {"unavailable": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def time_to_target(ctx, capi, n, target, R, rng_kind, args):
-    """Wall time from solver creation to the first replica at the target."""
-    times, censored = [], 0
-    for s in range(args.tts_seeds):
-        params = capi.memetic_params(target_energy=target, rng_kind=rng_kind,
-                                     max_seconds=args.tts_limit)
-        t0 = time.perf_counter()
-        sv = capi.Solver(ctx, n, R, base_seed=1000 * (s + 1), params=params)
-        sv.run(race=True)
-        st = sv.status()
-        dt = time.perf_counter() - t0
-        if st["best_energy"] <= target:
-            times.append(dt)
-        else:
-            censored += 1
-        sv.close()
-    return {"n": n, "target": target, "seeds": args.tts_seeds, "censored": censored,
-            "limit_s": args.tts_limit, "times_s": times,
-            "median_s": statistics.median(times) if times else None,
-            "paper_a100_fit_s": 8.23e-8 * 1.313 ** n}
+def time_to_target(ctx, n, target, R, rng_kind, args):
+    """run_tts (fit.cpp:15-41) at one n: `--tts-samples` fresh replica sets
+    from disjoint seed blocks base + run * R, wall time from solver creation
+    to the first replica at the target (censored at --tts-limit)."""
+    from paper_2504_00987_b200.tts import quantile, run_tts
+    recs = run_tts(ctx, [n], {n: target}, reps=args.tts_samples, replicas=R,
+                   base_seed=100_000, time_limit=args.tts_limit, rng_kind=rng_kind)
+    times = [r["runtime"] for r in recs if r["reachedTarget"]]
+    a, b = PAPER_A100_FIT
+    return {"n": n, "target": target, "samples": len(recs),
+            "censored": sum(not r["reachedTarget"] for r in recs),
+            "limit_s": args.tts_limit, "replicas": R,
+            "seed_blocks": "base 100000 + run * replicas (disjoint; fit.cpp:30-31)",
+            "median_s": quantile(times, 0.5) if times else None,
+            "q1_s": quantile(times, 0.25) if times else None,
+            "q3_s": quantile(times, 0.75) if times else None,
+            "samples_detail": [{k: r[k] for k in ("seed", "runtime", "reachedTarget", "bestE",
+                                                  "bestSeq", "bestReplica")} for r in recs],
+            "paper_a100_fit_s": a * b ** n}
 
 
 if __name__ == "__main__":

@@ -47,6 +47,8 @@ extern "C" {
 
 #define LABS_MAX_N 256 /* device walkers hold n <= 256 (8 slots x 32 lanes) */
 #define LABS_MAX_WORDS 4
+#define LABS_MAX_PEERS 15 /* other islands' stop flags a solver can raise */
+#define LABS_IPC_HANDLE_BYTES 64 /* cudaIpcMemHandle_t */
 
 #define LABS_RNG_MT19937_64 0 /* reference-RNG mode (bit-exact trajectories) */
 #define LABS_RNG_PHILOX 1     /* production mode: counter-based Philox4x32-10 */
@@ -204,7 +206,9 @@ int labs_rng_seed_device(labs_ctx* ctx, int count, uint64_t base_seed,
 /* Replaces memetic_tabu(n, params, seed, stop, trace, replica_id)
  * (memetic.hpp:61-65; memetic.cpp:44-117). stop: optional host flag polled
  * once per memetic iteration (pass pinned/mapped memory or NULL). trace (may
- * be NULL): up to trace_cap records, *trace_len receives the count. */
+ * be NULL): up to trace_cap records are stored; *trace_len receives the
+ * number of records the run produced, which exceeds trace_cap when the
+ * trace was truncated (never silently: compare the two). */
 int labs_memetic(labs_ctx* ctx, int n, const labs_memetic_params* params,
                  uint64_t seed, const volatile int32_t* stop, int replica_id,
                  labs_run_result* out, labs_memetic_record* trace,
@@ -214,12 +218,35 @@ int labs_memetic(labs_ctx* ctx, int n, const labs_memetic_params* params,
  * `replicas` replicas, replica r seeded base_seed + r, racing to the target
  * with a device-resident stop flag; result = strictly-lowest energy, first
  * publisher keeps a tie. per_replica (may be NULL): replicas results.
- * traces (may be NULL): replicas x trace_cap records, trace_len: replicas. */
+ * traces (may be NULL): replicas x trace_cap records, trace_len: replicas
+ * (records produced per replica; > trace_cap means truncated, as for
+ * labs_memetic). */
 int labs_run_replicas(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
                       const labs_memetic_params* params, labs_run_result* out,
                       labs_run_result* per_replica,
                       labs_memetic_record* traces, int64_t trace_cap,
                       int64_t* trace_len);
+
+/* run_replicas over several GPUs of one node from one host thread (the
+ * multi-GPU form SURVEY.md §8b proposes; configs[4]'s island model without
+ * migration). The global replicas [0, replicas) are cut into ngpu
+ * contiguous blocks (sizes differ by at most one, larger blocks first);
+ * block g runs on ctxs[g], replica r keeps seed base_seed + r
+ * (parallel.cpp:38), so every replica's trajectory is the one it has on one
+ * GPU or in the reference until a stop fires. Stop: when every pair of
+ * devices has peer access, each GPU's stop flag is raised by the winning
+ * replica directly over NVLink (P2P stores, no host in the loop);
+ * otherwise the host forwards it between 10 ms epochs. Result: strictly
+ * lowest energy; ties go to the earlier publisher (one global publish
+ * counter when the devices have native P2P atomics, else (order, block)).
+ * ctxs may repeat a device (two islands sharing one GPU). per_replica,
+ * traces and trace_len are indexed by global replica as in
+ * labs_run_replicas. */
+int labs_run_replicas_multi(labs_ctx* const* ctxs, int ngpu, int n, int replicas,
+                            uint64_t base_seed, const labs_memetic_params* params,
+                            labs_run_result* out, labs_run_result* per_replica,
+                            labs_memetic_record* traces, int64_t trace_cap,
+                            int64_t* trace_len);
 
 /* ------------------------------------------- solver (epoch-driven K4) ---- */
 /* Device-resident replica set for long runs, throughput measurement and the
@@ -265,6 +292,23 @@ int labs_solver_export_elites(labs_solver* s, int k, uint64_t* d_words,
 int labs_solver_import_elites(labs_solver* s, int count,
                               const uint64_t* d_words,
                               const int64_t* d_energies, int rotation);
+/* Cross-island stop (the device-resident stop flag of SURVEY.md §8e).
+ * stop_flag: device address of this solver's int32 stop flag (a plain
+ * cudaMalloc allocation, so labs_ipc_export can share it with other
+ * processes). set_peer_stops: up to LABS_MAX_PEERS flags, valid in this
+ * process (another device's flag with peer access enabled, or one opened by
+ * labs_ipc_open), that a replica reaching the target raises together with
+ * its own (proj/src/parallel.cpp:40 request_stop, across GPUs over NVLink);
+ * count = 0 clears them. */
+int labs_solver_stop_flag(labs_solver* s, int32_t** d_flag);
+int labs_solver_set_peer_stops(labs_solver* s, int count, int32_t* const* d_flags);
+/* CUDA IPC for the multi-process island model: export a device allocation
+ * made by this library (e.g. a stop flag) as LABS_IPC_HANDLE_BYTES opaque
+ * bytes; open a handle exported by another process (on ctx's device, peer
+ * access enabled lazily); close what was opened. */
+int labs_ipc_export(labs_ctx* ctx, const void* d_ptr, void* handle);
+int labs_ipc_open(labs_ctx* ctx, const void* handle, void** d_ptr);
+int labs_ipc_close(labs_ctx* ctx, void* d_ptr);
 /* Copy every population out (host buffers, synchronizing): words
  * replicas x K x ceil(n/64), energies replicas x K. For inspection and
  * checkpointing between epochs. */
@@ -272,9 +316,11 @@ int labs_solver_population(labs_solver* s, uint64_t* words, int32_t* energies);
 /* Checkpoint / resume for long runs: the complete replica state (populations,
  * energies, bests, counters, RNG states, traces) as one host blob.
  * state_size returns the byte count; load requires a solver created with the
- * same n, replicas, params and trace_cap (checked; LABS_ERR_INVALID_ARGUMENT
- * otherwise). A resumed run continues every replica's trajectory exactly;
- * max_seconds budgets restart from the load time. */
+ * same n, replicas, base_seed, replica_offset, trace_cap and every field of
+ * params (checked; LABS_ERR_INVALID_ARGUMENT otherwise). A resumed run
+ * continues every replica's trajectory exactly; each replica's elapsed time
+ * is saved, so max_seconds budgets and reported wall times continue from
+ * the checkpoint. */
 int64_t labs_solver_state_size(labs_solver* s);
 int labs_solver_save(labs_solver* s, void* blob);
 int labs_solver_load(labs_solver* s, const void* blob);
@@ -293,9 +339,13 @@ int labs_local_optima(labs_ctx* ctx, int n, int64_t* count);
 
 /* ------------------------------------------------------- diagnostics --- */
 /* Measured INT32 lane-instruction rate of this device (IMAD on the FMA pipe
- * alongside IADD3/LOP3 on the ALU pipe), in Gop/s: the roofline denominator
- * bench.py reports the integer-bound walker against. */
+ * alongside IADD3/LOP3 on the ALU pipe), in Gop/s: the issue ceiling of
+ * every integer instruction the walker executes (both pipes). */
 int labs_bench_int_peak(labs_ctx* ctx, double* gops);
+/* Measured IMAD-only rate (INT32 multiply-adds on the FMA pipe alone), in
+ * Gop/s: the denominator of SURVEY.md §8(d)'s lag-term roofline ((N-1) MACs
+ * per flip-evaluation). */
+int labs_bench_imad_peak(labs_ctx* ctx, double* gmacs);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,8 @@ LABS_ERR_RUNTIME = 3
 LABS_ERR_CUDA = 4
 LABS_MAX_N = 256
 LABS_MAX_WORDS = 4
+LABS_MAX_PEERS = 15
+LABS_IPC_HANDLE_BYTES = 64
 RNG_MT19937_64 = 0
 RNG_PHILOX = 1
 TIE_REFERENCE = 0
@@ -46,6 +48,8 @@ EXPORTS = [
     "labs_solver_results", "labs_solver_export_elites", "labs_solver_import_elites",
     "labs_bench_int_peak", "labs_exhaustive_optimum", "labs_local_optima",
     "labs_solver_population", "labs_solver_state_size", "labs_solver_save", "labs_solver_load",
+    "labs_solver_stop_flag", "labs_solver_set_peer_stops", "labs_ipc_export", "labs_ipc_open",
+    "labs_ipc_close", "labs_run_replicas_multi", "labs_bench_imad_peak",
 ]
 CROSSOVER_UNIFORM = 0
 CROSSOVER_ONE_POINT = 1
@@ -181,6 +185,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.labs_solver_import_elites.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                             C.c_int]
     L.labs_bench_int_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.labs_bench_imad_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     L.labs_exhaustive_optimum.argtypes = [C.c_void_p, C.c_int, i64p, u64p, C.c_int64, i64p]
     L.labs_local_optima.argtypes = [C.c_void_p, C.c_int, i64p]
     L.labs_solver_population.argtypes = [C.c_void_p, u64p, i32p]
@@ -188,6 +193,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.labs_solver_state_size.restype = C.c_int64
     L.labs_solver_save.argtypes = [C.c_void_p, C.c_void_p]
     L.labs_solver_load.argtypes = [C.c_void_p, C.c_void_p]
+    L.labs_solver_stop_flag.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    L.labs_solver_set_peer_stops.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.labs_ipc_export.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    L.labs_ipc_open.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.labs_ipc_close.argtypes = [C.c_void_p, C.c_void_p]
+    L.labs_run_replicas_multi.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
+                                          C.c_uint64, C.POINTER(MemeticParams),
+                                          C.POINTER(RunResult), C.POINTER(RunResult),
+                                          C.POINTER(MemeticRecord), C.c_int64, i64p]
     _lib = L
     return L
 
@@ -270,6 +284,21 @@ class Context:
     def synchronize(self):
         _check(self.L.labs_ctx_synchronize(self.h))
 
+    # -- CUDA IPC (multi-process island stop flags) -------------------------
+    def ipc_export(self, d_ptr: int) -> bytes:
+        h = (C.c_ubyte * LABS_IPC_HANDLE_BYTES)()
+        _check(self.L.labs_ipc_export(self.h, C.c_void_p(d_ptr), h))
+        return bytes(h)
+
+    def ipc_open(self, handle: bytes) -> int:
+        h = (C.c_ubyte * LABS_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+        p = C.c_void_p()
+        _check(self.L.labs_ipc_open(self.h, h, C.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, d_ptr: int):
+        _check(self.L.labs_ipc_close(self.h, C.c_void_p(d_ptr)))
+
     # -- K5 ---------------------------------------------------------------
     def exhaustive_optimum(self, n: int, cap: int = 1 << 16):
         """(optimal E, raw optimal sequences with s_0 = +1) by full enumeration."""
@@ -287,9 +316,15 @@ class Context:
         return int(c.value)
 
     def int_peak_gops(self) -> float:
-        """Measured INT32 lane-instruction rate (roofline denominator)."""
+        """Measured INT32 lane-instruction rate, both integer pipes."""
         g = C.c_double(0)
         _check(self.L.labs_bench_int_peak(self.h, C.byref(g)))
+        return float(g.value)
+
+    def imad_peak_gops(self) -> float:
+        """Measured IMAD-only rate (the §8(d) lag-term roofline denominator)."""
+        g = C.c_double(0)
+        _check(self.L.labs_bench_imad_peak(self.h, C.byref(g)))
         return float(g.value)
 
     # -- K1 ---------------------------------------------------------------
@@ -393,7 +428,7 @@ class Context:
         d = _result(out, n)
         if trace_cap:
             d["trace"] = [(int(tr[i].iteration), bool(tr[i].stop_seen), int(tr[i].child_energy))
-                          for i in range(tl.value)]
+                          for i in range(min(tl.value, trace_cap))]
         return d
 
     def run_replicas(self, n: int, replicas: int, base_seed: int,
@@ -413,8 +448,33 @@ class Context:
                 reps[r]["trace"] = [(int(tr[r * trace_cap + i].iteration),
                                      bool(tr[r * trace_cap + i].stop_seen),
                                      int(tr[r * trace_cap + i].child_energy))
-                                    for i in range(int(tl[r]))]
+                                    for i in range(min(int(tl[r]), trace_cap))]
         return res, reps
+
+
+def run_replicas_multi(ctxs, n: int, replicas: int, base_seed: int,
+                       params: MemeticParams | None = None, trace_cap: int = 0):
+    """labs_run_replicas_multi: one host thread, len(ctxs) GPUs (contexts may
+    share a device), contiguous replica blocks, device-side cross-GPU stop."""
+    params = params or memetic_params()
+    L = load_library()
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    out = RunResult()
+    per = (RunResult * replicas)()
+    tr = (MemeticRecord * (replicas * max(trace_cap, 1)))() if trace_cap else None
+    tl = np.zeros(replicas, dtype=np.int64)
+    _check(L.labs_run_replicas_multi(arr, len(ctxs), n, replicas, C.c_uint64(base_seed),
+                                     C.byref(params), C.byref(out), per, tr, trace_cap,
+                                     _ptr(tl, i64p) if trace_cap else None))
+    res = _result(out, n)
+    reps = [_result(per[i], n) for i in range(replicas)]
+    if trace_cap:
+        for r in range(replicas):
+            reps[r]["trace"] = [(int(tr[r * trace_cap + i].iteration),
+                                 bool(tr[r * trace_cap + i].stop_seen),
+                                 int(tr[r * trace_cap + i].child_energy))
+                                for i in range(min(int(tl[r]), trace_cap))]
+    return res, reps
 
 
 class Solver:
@@ -482,7 +542,7 @@ class Solver:
                 r["trace"] = [(int(tr[i * self.trace_cap + j].iteration),
                                bool(tr[i * self.trace_cap + j].stop_seen),
                                int(tr[i * self.trace_cap + j].child_energy))
-                              for j in range(int(tl[i]))]
+                              for j in range(min(int(tl[i]), self.trace_cap))]
         return reps
 
     def population(self):
@@ -504,6 +564,19 @@ class Solver:
         """Resume from a checkpoint made by a solver with the same setup."""
         buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
         _check(self.L.labs_solver_load(self.h, buf))
+
+    @property
+    def stop_flag(self) -> int:
+        """Device address of this solver's stop flag (IPC-exportable)."""
+        p = C.c_void_p()
+        _check(self.L.labs_solver_stop_flag(self.h, C.byref(p)))
+        return int(p.value)
+
+    def set_peer_stops(self, d_flags):
+        """Flags (device pointers valid in this process) a replica reaching
+        the target raises together with its own."""
+        arr = (C.c_void_p * max(len(d_flags), 1))(*[C.c_void_p(int(f)) for f in d_flags])
+        _check(self.L.labs_solver_set_peer_stops(self.h, len(d_flags), arr))
 
     def export_elites(self, k: int, d_words: int, d_energies: int):
         _check(self.L.labs_solver_export_elites(self.h, k, C.c_void_p(d_words),

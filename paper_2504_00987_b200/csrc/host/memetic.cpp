@@ -50,19 +50,7 @@ Sequence mutate(const Sequence& child, double p_mutate, Rng& rng) {
 
 RunResult memetic_tabu(int n, const MemeticParams& params, std::uint64_t seed,
                        const std::atomic<bool>* stop, MemeticTrace* trace, int replica_id) {
-  if (n < 2) throw std::invalid_argument("memetic needs length >= 2");
-  if (params.scan_workers < 1) throw std::invalid_argument("scan workers must be >= 1");
-  labs_memetic_params p{};
-  p.population_size = params.population_size;
-  p.rng_kind = LABS_RNG_MT19937_64;
-  p.p_comb = params.p_comb;
-  p.p_mutate = params.p_mutate.value_or(-1.0);
-  if (params.p_mutate && !(*params.p_mutate > 0.0))
-    throw std::invalid_argument("mutation probability must be in (0, 1]");
-  p.target_energy = params.target_energy;
-  p.max_seconds = params.max_seconds.value_or(-1.0);
-  p.max_iterations = params.max_iterations.value_or(-1);
-  p.tabu = {params.tabu.min_tabu_factor, params.tabu.max_tabu_factor, LABS_TIE_REFERENCE, 0};
+  const labs_memetic_params p = detail::device_params(n, params);
 
   // The device polls an int32 flag between epochs; mirror the caller's
   // atomic<bool> into it while the run is in flight.
@@ -79,7 +67,7 @@ RunResult memetic_tabu(int n, const MemeticParams& params, std::uint64_t seed,
     });
   }
   labs_run_result out{};
-  const int64_t cap = trace ? (params.max_iterations ? *params.max_iterations + 1 : 1 << 20) : 0;
+  const int64_t cap = trace ? detail::trace_capacity(params, 1 << 20) : 0;
   std::vector<labs_memetic_record> recs(trace ? cap : 0);
   int64_t len = 0;
   const int rc = labs_memetic(detail::device(), n, &p, seed, stop ? &flag : nullptr, replica_id,
@@ -87,6 +75,7 @@ RunResult memetic_tabu(int n, const MemeticParams& params, std::uint64_t seed,
   done.store(true, std::memory_order_release);
   if (watcher.joinable()) watcher.join();
   detail::check(rc);
+  if (trace) detail::check_trace_len(len, cap);
   RunResult r;
   r.best = Sequence(n);
   for (int w = 0; w < r.best.word_count(); ++w) r.best.set_word(w, out.best[w]);

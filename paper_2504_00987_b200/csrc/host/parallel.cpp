@@ -1,4 +1,5 @@
-// labsolve::run_replicas on the B200 (labs_run_replicas), plus the host-side
+// labsolve::run_replicas on the B200 (labs_run_replicas, or
+// labs_run_replicas_multi over the GPUs in LABS_DEVICES), plus the host-side
 // SharedState and the paper's sizing helpers.
 #include "labsolve/parallel.hpp"
 
@@ -24,28 +25,28 @@ std::optional<RunResult> SharedState::best() const {
 RunResult run_replicas(const ParallelConfig& cfg, ReplicaReport* report) {
   if (cfg.n < 2) throw std::invalid_argument("run needs length >= 2");
   if (cfg.replicas < 1) throw std::invalid_argument("replicas must be >= 1");
-  const MemeticParams& m = cfg.memetic;
-  if (m.scan_workers < 1) throw std::invalid_argument("scan workers must be >= 1");
-  labs_memetic_params p{};
-  p.population_size = m.population_size;
-  p.rng_kind = LABS_RNG_MT19937_64;
-  p.p_comb = m.p_comb;
-  p.p_mutate = m.p_mutate.value_or(-1.0);
-  if (m.p_mutate && !(*m.p_mutate > 0.0))
-    throw std::invalid_argument("mutation probability must be in (0, 1]");
-  p.target_energy = m.target_energy;
-  p.max_seconds = m.max_seconds.value_or(-1.0);
-  p.max_iterations = m.max_iterations.value_or(-1);
-  p.tabu = {m.tabu.min_tabu_factor, m.tabu.max_tabu_factor, LABS_TIE_REFERENCE, 0};
+  const labs_memetic_params p = detail::device_params(cfg.n, cfg.memetic);
   const bool traces = report && report->collect_traces;
-  const int64_t cap = traces ? (m.max_iterations ? *m.max_iterations + 1 : 1 << 16) : 0;
+  // Bounded runs keep every record; unbounded ones get 4096 per replica and
+  // throw (never truncate) if a replica produced more.
+  const int64_t cap = traces ? detail::trace_capacity(cfg.memetic, 4096) : 0;
   std::vector<labs_memetic_record> recs(traces ? cap * cfg.replicas : 0);
   std::vector<int64_t> lens(traces ? cfg.replicas : 0);
   std::vector<labs_run_result> per(cfg.replicas);
   labs_run_result best{};
-  detail::check(labs_run_replicas(detail::device(), cfg.n, cfg.replicas, cfg.base_seed, &p,
-                                  &best, per.data(), traces ? recs.data() : nullptr, cap,
-                                  traces ? lens.data() : nullptr));
+  // One GPU, or every GPU in LABS_DEVICES (contiguous replica blocks, seeds
+  // base_seed + r either way; labs_run_replicas_multi).
+  const std::vector<labs_ctx*>& ctxs = detail::devices();
+  if (ctxs.size() > 1)
+    detail::check(labs_run_replicas_multi(ctxs.data(), static_cast<int>(ctxs.size()), cfg.n,
+                                          cfg.replicas, cfg.base_seed, &p, &best, per.data(),
+                                          traces ? recs.data() : nullptr, cap,
+                                          traces ? lens.data() : nullptr));
+  else
+    detail::check(labs_run_replicas(ctxs.front(), cfg.n, cfg.replicas, cfg.base_seed, &p, &best,
+                                    per.data(), traces ? recs.data() : nullptr, cap,
+                                    traces ? lens.data() : nullptr));
+  for (int r = 0; traces && r < cfg.replicas; ++r) detail::check_trace_len(lens[r], cap);
   auto convert = [&](const labs_run_result& o) {
     RunResult r;
     r.best = Sequence(cfg.n);

@@ -1,10 +1,7 @@
-// labs_kernels.cu — sm_100a kernels K1..K4 and the C ABI (include/labs_b200.h).
-//
-// Every kernel is warp-per-walker (or warp-per-replica): 4 independent warps
-// per 128-thread block, no block-level barriers, each warp with a private
-// slice of dynamic shared memory (WalkSmem + optional mt19937_64 state).
-// Kernels are templated on NS = ceil(n/32) so the per-slot register arrays
-// are fully unrolled; the host dispatches NS in [1, 8] (n <= 256).
+// labs_kernels.cu — the C ABI (include/labs_b200.h) over the sm_100a
+// kernels: argument checks, device buffers, NS dispatch to the per-NS
+// launchers (labs_ns.cu), the epoch-driven solver, checkpoints, the
+// multi-GPU run and the island kernels. K5 lives in labs_exhaust.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,273 +13,9 @@
 #include <string>
 #include <vector>
 
-#include "labs_b200.h"
-#include "labs_exhaustive.cuh"
-#include "labs_memetic.cuh"
-#include "labs_walker.cuh"
+#include "labs_host.cuh"
 
 namespace labsk {
-
-constexpr int kWarps = 4;  // walkers per block
-
-// Occupancy target. The walker is issue-bound (ncu: ~89% issue slots busy),
-// so registers matter more than warps: 6 blocks (24 warps) per SM up to
-// n = 128 caps registers at 85/thread, which removed the smem-base
-// rematerialization of the 64-register build (+7% at n=64, +12% at n=119,
-// measured); longer sequences carry twice the per-slot state.
-#ifndef LABS_MINB_SMALL
-#define LABS_MINB_SMALL 6
-#endif
-#ifndef LABS_MINB_LARGE
-#define LABS_MINB_LARGE 4
-#endif
-template <int NS>
-__host__ __device__ constexpr int min_blocks() {
-  return NS <= 4 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
-}
-
-// Shared memory of one walker (tile): RNG block, cold replica bookkeeping,
-// walker vectors.
-template <int L, bool MT>
-struct TileSlot {
-  uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
-  uint64_t out[MT ? kMtN : PhiloxRng::kBlock];  // tempered block / Philox block
-  TileCtl ctl;
-  WalkSmemL<L> walk;
-};
-
-template <int L, bool MT>
-__host__ __device__ constexpr size_t tile_slot_bytes() {
-  return (sizeof(TileSlot<L, MT>) + 15) & ~size_t(15);
-}
-
-// Tile t of the block owns slot t; T = 32 is the warp-per-walker kernels'.
-template <int L, bool MT, int T>
-__device__ __forceinline__ TileSlot<L, MT>& my_tile_slot() {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  return *reinterpret_cast<TileSlot<L, MT>*>(smem_raw +
-                                             (threadIdx.x / T) * tile_slot_bytes<L, MT>());
-}
-
-template <int NS, bool MT>
-__host__ __device__ constexpr size_t slot_bytes() {
-  return tile_slot_bytes<32 * NS, MT>();
-}
-
-template <int NS, bool MT>
-__device__ __forceinline__ TileSlot<32 * NS, MT>& my_slot() {
-  return my_tile_slot<32 * NS, MT, 32>();
-}
-
-__device__ __forceinline__ int global_warp() {
-  return blockIdx.x * kWarps + (threadIdx.x >> 5);
-}
-__device__ __forceinline__ int total_warps() { return gridDim.x * kWarps; }
-
-// Load an engine state into the tile's slot and bind `rng` to it.
-template <int T = 32>
-__device__ __forceinline__ void mt_load(uint64_t* s, uint64_t* out, const labs_rng_state& g,
-                                        MtRngT<T>& rng) {
-  for (int i = tile_lane<T>(); i < kMtN; i += T) s[i] = g.mt[i];
-  tile_sync<T>();
-  mt_temper_all<T>(s, out);
-  rng.bind(s, out, g.idx);
-}
-template <int T = 32>
-__device__ __forceinline__ void mt_store(const uint64_t* s, labs_rng_state& g,
-                                         int idx) {
-  tile_sync<T>();
-  for (int i = tile_lane<T>(); i < kMtN; i += T) g.mt[i] = s[i];
-  if (tile_lane<T>() == 0) g.idx = idx;
-  tile_sync<T>();
-}
-
-// ------------------------------------------------------------------ K1 --
-template <int NS>
-__global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>())
-k_build(int n, int count, const uint64_t* __restrict__ words,
-        int32_t* __restrict__ corr, int64_t* __restrict__ energy,
-        int64_t* __restrict__ nbr) {
-  auto& sl = my_slot<NS, false>();
-  smem_clear(sl.walk);
-  Walker<NS> w;
-  w.sm = &sl.walk;
-  const int nw = (n + 63) / 64;
-  for (int item = global_warp(); item < count; item += total_warps()) {
-    uint32_t in[NS];
-    load_chunks<NS>(words + static_cast<size_t>(item) * nw, nw, in);
-    w.init(n, in);
-    int dE[NS];
-    w.delta(dE);
-#pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + lane_id();
-      if (j < n && nbr) nbr[static_cast<size_t>(item) * n + j] = w.E + dE[b];
-      if (j >= 1 && j < n && corr)
-        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.CK[b];
-    }
-    if (lane_id() == 0) energy[item] = w.E;
-    __syncwarp();
-  }
-}
-
-// ----------------------------------------------------------------- K2b --
-template <int NS>
-__global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>())
-k_flip_trace(int n, int count, const uint64_t* __restrict__ words, int flips,
-             const int32_t* __restrict__ positions, int64_t* __restrict__ energy,
-             int64_t* __restrict__ nbr) {
-  auto& sl = my_slot<NS, false>();
-  smem_clear(sl.walk);
-  Walker<NS> w;
-  w.sm = &sl.walk;
-  const int nw = (n + 63) / 64;
-  for (int item = global_warp(); item < count; item += total_warps()) {
-    uint32_t in[NS];
-    load_chunks<NS>(words + static_cast<size_t>(item) * nw, nw, in);
-    w.init(n, in);
-    for (int f = 0; f < flips; ++f) {
-      const int pos = positions[static_cast<size_t>(item) * flips + f];
-      int dE[NS];
-      w.delta(dE);
-      const int dEp = at_position<NS>(dE, pos);
-      w.apply(pos, dEp, f + 1, 0);
-      if (lane_id() == 0) energy[static_cast<size_t>(item) * flips + f] = w.E;
-      if (nbr) {
-        w.delta(dE);
-#pragma unroll
-        for (int b = 0; b < NS; ++b) {
-          const int j = 32 * b + lane_id();
-          if (j < n)
-            nbr[(static_cast<size_t>(item) * flips + f) * n + j] = w.E + dE[b];
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ K2 --
-template <int NS>
-__global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>())
-k_scan(int n, int count, const uint64_t* __restrict__ words,
-       const uint8_t* __restrict__ admissible, labs_rng_state* rng_states,
-       int allow_fallback, int tie_rule, int32_t* pos_out, int64_t* e_out,
-       int32_t* fb_out, int32_t* ntie_out, uint64_t* tie_out) {
-  auto& sl = my_slot<NS, true>();
-  smem_clear(sl.walk);
-  Walker<NS> w;
-  w.sm = &sl.walk;
-  const int nw = (n + 63) / 64;
-  for (int item = global_warp(); item < count; item += total_warps()) {
-    MtRng rng;
-    mt_load(sl.mt, sl.out, rng_states[item], rng);
-    uint32_t in[NS];
-    load_chunks<NS>(words + static_cast<size_t>(item) * nw, nw, in);
-    w.init(n, in);
-    int dE[NS];
-    bool adm[NS];
-    w.delta(dE);
-    bool any = false;
-#pragma unroll
-    for (int b = 0; b < NS; ++b) {
-      const int j = 32 * b + lane_id();
-      adm[b] = j < n && admissible[static_cast<size_t>(item) * n + j] != 0;
-      any |= adm[b];
-    }
-    any = __any_sync(kFull, any);
-    int pos = -1, dEp = 0, fb = 0, ntie = 0;
-    uint32_t msk[NS];
-#pragma unroll
-    for (int b = 0; b < NS; ++b) msk[b] = 0u;
-    if (any || allow_fallback)
-      select_move<NS, 32, true>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
-    if (lane_id() == 0) {
-      pos_out[item] = pos;
-      e_out[item] = pos >= 0 ? static_cast<int64_t>(w.E) + dEp : 0;
-      fb_out[item] = fb;
-      ntie_out[item] = ntie;
-      if (tie_out) {
-#pragma unroll
-        for (int wi = 0; wi < LABS_MAX_WORDS; ++wi) {
-          uint64_t lo = 2 * wi < NS ? msk[2 * wi] : 0u;
-          uint64_t hi = 2 * wi + 1 < NS ? msk[2 * wi + 1] : 0u;
-          tie_out[static_cast<size_t>(item) * LABS_MAX_WORDS + wi] = lo | (hi << 32);
-        }
-      }
-    }
-    mt_store(sl.mt, rng_states[item], rng.idx);
-    __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ K3 --
-struct WalkArgs {
-  int n, count, walks;
-  const uint64_t* start;
-  TabuCfg cfg;
-  labs_rng_state* mt;
-  uint64_t seed, ctr_base;
-  uint64_t* best;
-  int64_t* bestE;
-  int32_t* info;
-  StepRec* steps;
-  int steps_stride;
-  unsigned long long* iters;
-};
-
-template <int NS, bool MT>
-__global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_tabu(WalkArgs A) {
-  auto& sl = my_slot<NS, MT>();
-  smem_clear(sl.walk);
-  Walker<NS> w;
-  w.sm = &sl.walk;
-  const int n = A.n, nw = (n + 63) / 64;
-  unsigned long long total = 0;
-  for (int item = global_warp(); item < A.count; item += total_warps()) {
-    uint32_t cur[NS], best[NS];
-    load_chunks<NS>(A.start + static_cast<size_t>(item) * nw, nw, cur);
-    int bestE = 0;
-    if constexpr (MT) {
-      MtRng rng;
-      mt_load(sl.mt, sl.out, A.mt[item], rng);
-      for (int k = 0; k < A.walks; ++k) {
-        int steps = 0;
-        bestE = tabu_walk<NS>(w, n, cur, rng, A.cfg, best,
-                              A.info ? A.info + 3 * static_cast<size_t>(item) : nullptr,
-                              A.steps ? A.steps + static_cast<size_t>(item) * A.steps_stride
-                                      : nullptr,
-                              &steps);
-        total += steps;
-#pragma unroll
-        for (int b = 0; b < NS; ++b) cur[b] = best[b];
-      }
-      mt_store(sl.mt, A.mt[item], rng.idx);
-    } else {
-      PhiloxRng rng;
-      rng.k0 = static_cast<uint32_t>(A.seed);
-      rng.k1 = static_cast<uint32_t>(A.seed >> 32);
-      rng.s0 = static_cast<uint32_t>(item);
-      rng.s1 = 0x4C414253u;  // "LABS"
-      rng.bind(sl.out, A.ctr_base);
-      for (int k = 0; k < A.walks; ++k) {
-        int steps = 0;
-        bestE = tabu_walk<NS>(w, n, cur, rng, A.cfg, best,
-                              A.info ? A.info + 3 * static_cast<size_t>(item) : nullptr,
-                              A.steps ? A.steps + static_cast<size_t>(item) * A.steps_stride
-                                      : nullptr,
-                              &steps);
-        total += steps;
-#pragma unroll
-        for (int b = 0; b < NS; ++b) cur[b] = best[b];
-      }
-    }
-    store_chunks<NS>(A.best + static_cast<size_t>(item) * nw, nw, best);
-    if (lane_id() == 0) A.bestE[item] = bestE;
-    __syncwarp();
-  }
-  if (A.iters && lane_id() == 0 && total) atomicAdd(A.iters, total);
-}
 
 __global__ void k_seed(int count, uint64_t base, labs_rng_state* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -296,81 +29,6 @@ __global__ void k_seed(int count, uint64_t base, labs_rng_state* out) {
   out[c].idx = kMtN;
   out[c].pad_ = 0;
 }
-
-// ------------------------------------------------------------------ K4 --
-// Replica RNG binding for memetic_tiles: mt19937_64 state copied between the
-// replica's global record and the tile's shared slot, or the Philox stream
-// (key = base seed, stream = global replica id) positioned at its counter.
-template <int T>
-struct MtBind {
-  labs_rng_state* g;
-  uint64_t* mt;
-  uint64_t* out;
-  __device__ __forceinline__ void load(int r, MtRngT<T>& rng) { mt_load<T>(mt, out, g[r], rng); }
-  __device__ __forceinline__ void save(int r, MtRngT<T>& rng) { mt_store<T>(mt, g[r], rng.idx); }
-};
-template <int T>
-struct PhiloxBind {
-  uint64_t* ctr;
-  uint64_t* buf;
-  int64_t offset;
-  __device__ __forceinline__ void load(int r, PhiloxRngT<T>& rng) {
-    rng.s0 = static_cast<uint32_t>(offset + r);
-    rng.bind(buf, ctr[r]);
-  }
-  __device__ __forceinline__ void save(int r, PhiloxRngT<T>& rng) {
-    if (tile_lane<T>() == 0) ctr[r] = rng.ctr;
-    tile_sync<T>();
-  }
-};
-
-// Replicas per tile of T lanes; T < 32 packs 32/T replicas into each warp
-// (labs_memetic.cuh: memetic_tiles).
-template <int NS, int T>
-__host__ __device__ constexpr int min_blocks_memetic() {
-  return T * NS <= 128 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
-}
-
-// The two policy switches (aspiration, tie rule) as template parameters, so
-// the tabu step carries no runtime policy tests.
-template <int NS, int T, class R, class RB>
-__device__ __forceinline__ void run_policy(const MemeticArgs& A, Walker<NS, T>& w, R& rng,
-                                           RB& rb, TileCtl& ctl) {
-  const bool ref_ties = A.tabu.tie_rule == LABS_TIE_REFERENCE;
-  if (A.tabu.aspiration) {
-    if (ref_ties) memetic_tiles<NS, T, true, true>(A, w, rng, rb, ctl);
-    else memetic_tiles<NS, T, true, false>(A, w, rng, rb, ctl);
-  } else {
-    if (ref_ties) memetic_tiles<NS, T, false, true>(A, w, rng, rb, ctl);
-    else memetic_tiles<NS, T, false, false>(A, w, rng, rb, ctl);
-  }
-}
-
-template <int NS, int T, bool MT>
-__global__ void __launch_bounds__(32 * kWarps, (min_blocks_memetic<NS, T>()))
-k_memetic(MemeticArgs A) {
-  constexpr int L = T * NS;
-  auto& sl = my_tile_slot<L, MT, T>();
-  smem_clear<L, T>(sl.walk);
-  Walker<NS, T> w;
-  w.sm = &sl.walk;
-  if constexpr (MT) {
-    MtRngT<T> rng;
-    rng.bind(sl.mt, sl.out, 0);  // valid until a replica is loaded
-    MtBind<T> rb{A.mt, sl.mt, sl.out};
-    run_policy<NS, T>(A, w, rng, rb, sl.ctl);
-  } else {
-    PhiloxRngT<T> rng;
-    rng.k0 = static_cast<uint32_t>(A.base_seed);
-    rng.k1 = static_cast<uint32_t>(A.base_seed >> 32);
-    rng.s0 = 0;
-    rng.s1 = 0x4D454D45u;  // "MEME"
-    rng.bind(sl.out, 0);  // valid until a replica is loaded
-    PhiloxBind<T> rb{A.ctr, sl.out, A.replica_offset};
-    run_policy<NS, T>(A, w, rng, rb, sl.ctl);
-  }
-}
-
 
 // ---------------------------------------------------- island exchange ----
 // Top-k replica bests, best first: k rounds of a block-wide argmin over the
@@ -465,139 +123,40 @@ __global__ void __launch_bounds__(256) k_int_peak(int iters, int seed, int* sink
   if (v == 0x7fffffff) sink[0] = v;  // keep the chains alive
 }
 
+// IMAD-only probe: the INT32 multiply-add rate alone (FMA pipe), the
+// denominator SURVEY.md §8(d) names for the lag-term MACs ((N-1) per
+// flip-evaluation). 8 independent IMAD chains per thread, register operands.
+__global__ void __launch_bounds__(256) k_imad_peak(int iters, int seed, int* sink) {
+  int a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = (threadIdx.x + i) ^ seed;
+    b[i] = (blockIdx.x + 3 * i) ^ seed;
+  }
+  const int m = seed | 1;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = a[i] * m + b[i];
+    }
+  }
+  int v = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v ^= a[i];
+  if (v == 0x7fffffff) sink[0] = v;
+}
+
 }  // namespace labsk
 
-// ====================================================================== ABI
 using namespace labsk;
+using namespace labsh;
 
-struct labs_ctx {
-  int device = 0;
-  int sm_count = 0;
-  cudaStream_t stream = nullptr;
-};
-
-namespace {
-
+namespace labsh {
 thread_local std::string g_err;
-
-int fail(int code, const std::string& msg) {
-  g_err = msg;
-  return code;
 }
 
-#define LABS_CUDA(call)                                                    \
-  do {                                                                     \
-    cudaError_t e_ = (call);                                               \
-    if (e_ != cudaSuccess)                                                 \
-      return fail(LABS_ERR_CUDA, std::string(#call) + ": " +               \
-                                     cudaGetErrorString(e_));              \
-  } while (0)
-
-int check_n(int n) {
-  if (n < 2) return fail(LABS_ERR_INVALID_ARGUMENT, "length must be >= 2");
-  if (n > LABS_MAX_N)
-    return fail(LABS_ERR_INVALID_ARGUMENT,
-                "length exceeds the device walker limit " +
-                    std::to_string(LABS_MAX_N));
-  return LABS_OK;
-}
-
-int ns_of(int n) { return (n + 31) / 32; }
-int nw_of(int n) { return (n + 63) / 64; }
-
-// RAII device buffer on the context stream.
-struct DBuf {
-  void* p = nullptr;
-  cudaStream_t s = nullptr;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  ~DBuf() {
-    if (p) cudaFreeAsync(p, s);
-  }
-  cudaError_t alloc(size_t bytes, cudaStream_t st) {
-    s = st;
-    if (bytes == 0) bytes = 16;
-    return cudaMallocAsync(&p, bytes, st);
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
-#define LABS_ALLOC(buf, bytes) LABS_CUDA((buf).alloc((bytes), ctx->stream))
-#define LABS_H2D(dst, src, bytes) \
-  LABS_CUDA(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, ctx->stream))
-#define LABS_D2H(dst, src, bytes) \
-  LABS_CUDA(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, ctx->stream))
-
-template <class Kern>
-int grid_for(labs_ctx* ctx, Kern kern, size_t smem, int items, int* grid,
-             int per_block = kWarps) {
-  int per_sm = 0;
-  LABS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kWarps, smem));
-  if (per_sm < 1) per_sm = 1;
-  const int want = (items + per_block - 1) / per_block;
-  *grid = std::max(1, std::min(want, per_sm * ctx->sm_count));
-  return LABS_OK;
-}
-
-template <class Kern>
-int prep(Kern kern, size_t smem) {
-  if (smem > 48 * 1024)
-    LABS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  return LABS_OK;
-}
-
-// NS dispatch: calls f(std::integral_constant<int, NS>) for NS = ceil(n/32).
-template <class F>
-int dispatch(int n, F&& f) {
-  switch (ns_of(n)) {
-    case 1: return f(std::integral_constant<int, 1>{});
-    case 2: return f(std::integral_constant<int, 2>{});
-    case 3: return f(std::integral_constant<int, 3>{});
-    case 4: return f(std::integral_constant<int, 4>{});
-    case 5: return f(std::integral_constant<int, 5>{});
-    case 6: return f(std::integral_constant<int, 6>{});
-    case 7: return f(std::integral_constant<int, 7>{});
-    case 8: return f(std::integral_constant<int, 8>{});
-  }
-  return fail(LABS_ERR_INVALID_ARGUMENT, "unsupported length");
-}
-
-int check_tabu(const labs_tabu_params* p) {
-  if (!p) return fail(LABS_ERR_INVALID_ARGUMENT, "null tabu params");
-  if (p->min_tabu_factor < 0 || p->max_tabu_factor < p->min_tabu_factor ||
-      p->max_tabu_factor >= 1)
-    return fail(LABS_ERR_INVALID_ARGUMENT,
-                "tabu tenure factors need 0 <= min <= max < 1");
-  if (p->tie_rule != LABS_TIE_REFERENCE && p->tie_rule != LABS_TIE_LOWEST)
-    return fail(LABS_ERR_INVALID_ARGUMENT, "unknown tie rule");
-  return LABS_OK;
-}
-
-TabuCfg to_cfg(const labs_tabu_params* p) {
-  TabuCfg c;
-  c.min_factor = p->min_tabu_factor;
-  c.max_factor = p->max_tabu_factor;
-  c.tie_rule = p->tie_rule;
-  c.aspiration = p->aspiration ? 1 : 0;
-  return c;
-}
-
-int check_seq_padding(int n, int count, const uint64_t* words) {
-  const int nw = nw_of(n);
-  const int rem = n & 63;
-  if (!rem) return LABS_OK;
-  const uint64_t bad = ~((1ULL << rem) - 1ULL);
-  for (int c = 0; c < count; ++c)
-    if (words[static_cast<size_t>(c) * nw + nw - 1] & bad)
-      return fail(LABS_ERR_INVALID_ARGUMENT, "nonzero padding bits in sequence words");
-  return LABS_OK;
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -673,17 +232,9 @@ int labs_build_state(labs_ctx* ctx, int n, int count, const uint64_t* words,
   if (neighbor_out) LABS_ALLOC(dn, sizeof(int64_t) * count * n);
   LABS_H2D(dw.p, words, sizeof(uint64_t) * count * nw);
   int rc = dispatch(n, [&](auto ns) -> int {
-    constexpr int NS = decltype(ns)::value;
-    const size_t smem = kWarps * slot_bytes<NS, false>();
-    auto kern = k_build<NS>;
-    if (int r = prep(kern, smem)) return r;
-    int grid = 0;
-    if (int r = grid_for(ctx, kern, smem, count, &grid)) return r;
-    kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(n, count, dw.as<uint64_t>(),
-                                                   dc.as<int32_t>(), de.as<int64_t>(),
-                                                   neighbor_out ? dn.as<int64_t>() : nullptr);
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
+    return NsOps<decltype(ns)::value>::build(ctx, n, count, dw.as<uint64_t>(), dc.as<int32_t>(),
+                                             de.as<int64_t>(),
+                                             neighbor_out ? dn.as<int64_t>() : nullptr);
   });
   if (rc) return rc;
   if (corr_out) LABS_D2H(corr_out, dc.p, sizeof(int32_t) * count * (n - 1));
@@ -713,17 +264,9 @@ int labs_flip_trace(labs_ctx* ctx, int n, int count, const uint64_t* words, int 
   LABS_H2D(dw.p, words, sizeof(uint64_t) * count * nw);
   LABS_H2D(dp.p, positions, sizeof(int32_t) * count * flips);
   int rc = dispatch(n, [&](auto ns) -> int {
-    constexpr int NS = decltype(ns)::value;
-    const size_t smem = kWarps * slot_bytes<NS, false>();
-    auto kern = k_flip_trace<NS>;
-    if (int r = prep(kern, smem)) return r;
-    int grid = 0;
-    if (int r = grid_for(ctx, kern, smem, count, &grid)) return r;
-    kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(
-        n, count, dw.as<uint64_t>(), flips, dp.as<int32_t>(), de.as<int64_t>(),
-        neighbor_out ? dn.as<int64_t>() : nullptr);
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
+    return NsOps<decltype(ns)::value>::flip_trace(ctx, n, count, dw.as<uint64_t>(), flips,
+                                                  dp.as<int32_t>(), de.as<int64_t>(),
+                                                  neighbor_out ? dn.as<int64_t>() : nullptr);
   });
   if (rc) return rc;
   LABS_D2H(energy_out, de.p, sizeof(int64_t) * count * flips);
@@ -759,18 +302,10 @@ int labs_scan(labs_ctx* ctx, int n, int count, const uint64_t* words,
   LABS_H2D(da.p, admissible, static_cast<size_t>(count) * n);
   LABS_H2D(dr.p, rng, sizeof(labs_rng_state) * count);
   int rc = dispatch(n, [&](auto ns) -> int {
-    constexpr int NS = decltype(ns)::value;
-    const size_t smem = kWarps * slot_bytes<NS, true>();
-    auto kern = k_scan<NS>;
-    if (int r = prep(kern, smem)) return r;
-    int grid = 0;
-    if (int r = grid_for(ctx, kern, smem, count, &grid)) return r;
-    kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(
-        n, count, dw.as<uint64_t>(), da.as<uint8_t>(), dr.as<labs_rng_state>(),
+    return NsOps<decltype(ns)::value>::scan(
+        ctx, n, count, dw.as<uint64_t>(), da.as<uint8_t>(), dr.as<labs_rng_state>(),
         allow_fallback, tie_rule, dpos.as<int32_t>(), de.as<int64_t>(), dfb.as<int32_t>(),
         dnt.as<int32_t>(), dtm.as<uint64_t>());
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
   });
   if (rc) return rc;
   LABS_D2H(position, dpos.p, sizeof(int32_t) * count);
@@ -787,26 +322,7 @@ int labs_scan(labs_ctx* ctx, int n, int count, const uint64_t* words,
 }
 
 static int launch_tabu(labs_ctx* ctx, int n, WalkArgs& A, bool mt) {
-  return dispatch(n, [&](auto ns) -> int {
-    constexpr int NS = decltype(ns)::value;
-    if (mt) {
-      const size_t smem = kWarps * slot_bytes<NS, true>();
-      auto kern = k_tabu<NS, true>;
-      if (int r = prep(kern, smem)) return r;
-      int grid = 0;
-      if (int r = grid_for(ctx, kern, smem, A.count, &grid)) return r;
-      kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
-    } else {
-      const size_t smem = kWarps * slot_bytes<NS, false>();
-      auto kern = k_tabu<NS, false>;
-      if (int r = prep(kern, smem)) return r;
-      int grid = 0;
-      if (int r = grid_for(ctx, kern, smem, A.count, &grid)) return r;
-      kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
-    }
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
-  });
+  return dispatch(n, [&](auto ns) -> int { return NsOps<decltype(ns)::value>::tabu(ctx, A, mt); });
 }
 
 int labs_tabu_walks(labs_ctx* ctx, int n, int count, const uint64_t* start,
@@ -939,23 +455,6 @@ int dispatch_memetic(int n, F&& f) {
   return dispatch(n, [&](auto ns) -> int { return f(ns, std::integral_constant<int, 32>{}); });
 }
 
-template <int NS, int T, bool MT>
-constexpr size_t memetic_smem() {
-  return (32 / T) * kWarps * tile_slot_bytes<T * NS, MT>();
-}
-
-template <int NS, int T, bool MT>
-int launch_memetic(labs_ctx* ctx, const MemeticArgs& A) {
-  const size_t smem = memetic_smem<NS, T, MT>();
-  auto kern = k_memetic<NS, T, MT>;
-  if (int r = prep(kern, smem)) return r;
-  int grid = 0;
-  if (int r = grid_for(ctx, kern, smem, A.replicas, &grid, kWarps * (32 / T))) return r;
-  kern<<<grid, 32 * kWarps, smem, ctx->stream>>>(A);
-  LABS_CUDA(cudaGetLastError());
-  return LABS_OK;
-}
-
 }  // namespace
 
 // Device-resident replica set (include/labs_b200.h: labs_solver_*).
@@ -967,9 +466,18 @@ struct labs_solver {
   labs_memetic_params p{};
   bool mt = true;
   int64_t trace_cap = 0;
-  DBuf pop, popE, best, bestE, iters, status, init, t0, tend, order, counter, rng, ctr, stop,
+  DBuf pop, popE, best, bestE, iters, status, init, t0, tend, elapsed, order, counter, rng, ctr,
       tabu_total, tabu_rep, trace, trace_len, taken;
+  // The stop flag is a plain cudaMalloc allocation (not stream-ordered) so
+  // that other processes can map it through CUDA IPC (labs_ipc_export).
+  int32_t* stop = nullptr;
   MemeticArgs A{};
+  ~labs_solver() {
+    if (stop) {
+      cudaSetDevice(ctx->device);
+      cudaFree(stop);
+    }
+  }
 };
 
 extern "C" {
@@ -979,18 +487,11 @@ int labs_solver_capacity(labs_ctx* ctx, int n, int rng_kind) {
   int out = 0;
   cudaSetDevice(ctx->device);
   dispatch_memetic(n, [&](auto ns, auto tt) -> int {
-    constexpr int NS = decltype(ns)::value, T = decltype(tt)::value;
     int per_sm = 0;
-    if (rng_kind == LABS_RNG_MT19937_64) {
-      if (prep(k_memetic<NS, T, true>, memetic_smem<NS, T, true>())) return LABS_OK;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, T, true>, 32 * kWarps,
-                                                    memetic_smem<NS, T, true>());
-    } else {
-      if (prep(k_memetic<NS, T, false>, memetic_smem<NS, T, false>())) return LABS_OK;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_memetic<NS, T, false>, 32 * kWarps,
-                                                    memetic_smem<NS, T, false>());
-    }
-    out = per_sm * ctx->sm_count * kWarps * (32 / T);
+    if (MemeticOps<decltype(ns)::value, decltype(tt)::value>::blocks_per_sm(
+            ctx, rng_kind == LABS_RNG_MT19937_64, &per_sm))
+      return LABS_OK;
+    out = per_sm * ctx->sm_count * kWarps * (32 / decltype(tt)::value);
     return LABS_OK;
   });
   return out;
@@ -1027,9 +528,10 @@ int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   LABS_ALLOC(s->init, sizeof(int32_t) * R);
   LABS_ALLOC(s->t0, sizeof(int64_t) * R);
   LABS_ALLOC(s->tend, sizeof(int64_t) * R);
+  LABS_ALLOC(s->elapsed, sizeof(int64_t) * R);
   LABS_ALLOC(s->order, sizeof(int32_t) * R);
   LABS_ALLOC(s->counter, sizeof(int32_t));
-  LABS_ALLOC(s->stop, sizeof(int32_t));
+  LABS_CUDA(cudaMalloc(&s->stop, sizeof(int32_t)));
   LABS_ALLOC(s->tabu_total, sizeof(unsigned long long));
   LABS_ALLOC(s->tabu_rep, sizeof(int64_t) * R);
   LABS_ALLOC(s->taken, sizeof(int32_t) * R);
@@ -1044,7 +546,7 @@ int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   LABS_CUDA(cudaMemsetAsync(s->status.p, 0, sizeof(int32_t) * R, st));
   LABS_CUDA(cudaMemsetAsync(s->iters.p, 0, sizeof(int64_t) * R, st));
   LABS_CUDA(cudaMemsetAsync(s->counter.p, 0, sizeof(int32_t), st));
-  LABS_CUDA(cudaMemsetAsync(s->stop.p, 0, sizeof(int32_t), st));
+  LABS_CUDA(cudaMemsetAsync(s->stop, 0, sizeof(int32_t), st));
   LABS_CUDA(cudaMemsetAsync(s->tabu_total.p, 0, sizeof(unsigned long long), st));
   LABS_CUDA(cudaMemsetAsync(s->tabu_rep.p, 0, sizeof(int64_t) * R, st));
   LABS_CUDA(cudaMemsetAsync(s->order.p, 0xff, sizeof(int32_t) * R, st));
@@ -1087,7 +589,8 @@ int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   A.pub_counter = s->counter.as<int32_t>();
   A.mt = s->mt ? s->rng.as<labs_rng_state>() : nullptr;
   A.ctr = s->mt ? nullptr : s->ctr.as<uint64_t>();
-  A.stop = s->stop.as<int32_t>();
+  A.stop = s->stop;
+  A.npeers = 0;
   A.tabu_iters = s->tabu_total.as<unsigned long long>();
   A.tabu_per_replica = s->tabu_rep.as<int64_t>();
   A.trace = trace_cap ? s->trace.as<int64_t>() : nullptr;
@@ -1114,8 +617,7 @@ int labs_solver_run(labs_solver* s, int64_t epoch_iterations, double epoch_secon
   A.epoch_ns = epoch_seconds >= 0 ? static_cast<int64_t>(epoch_seconds * 1e9) : -1;
   A.race = race ? 1 : 0;
   return dispatch_memetic(s->n, [&](auto ns, auto tt) -> int {
-    constexpr int NS = decltype(ns)::value, T = decltype(tt)::value;
-    return s->mt ? launch_memetic<NS, T, true>(ctx, A) : launch_memetic<NS, T, false>(ctx, A);
+    return MemeticOps<decltype(ns)::value, decltype(tt)::value>::launch(ctx, A, s->mt);
   });
 }
 
@@ -1124,7 +626,7 @@ int labs_solver_request_stop(labs_solver* s) {
   labs_ctx* ctx = s->ctx;
   static const int32_t one = 1;
   LABS_CUDA(cudaSetDevice(ctx->device));
-  LABS_H2D(s->stop.p, &one, sizeof(int32_t));
+  LABS_H2D(s->stop, &one, sizeof(int32_t));
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
   return LABS_OK;
 }
@@ -1208,8 +710,10 @@ int labs_solver_results(labs_solver* s, labs_run_result* per_replica, labs_memet
     o.reached_target = bestE[r] <= s->p.target_energy;
     o.tabu_iterations = tabu[r];
     if (traces && s->trace_cap) {
+      // trace_len reports every record the replica produced; only the
+      // first trace_cap are stored, so a caller can detect truncation.
       const int64_t len = std::min(tl[r], s->trace_cap);
-      if (trace_len) trace_len[r] = len;
+      if (trace_len) trace_len[r] = tl[r];
       for (int64_t i = 0; i < len; ++i) {
         const int64_t* rec = &tr[(static_cast<size_t>(r) * s->trace_cap + i) * 3];
         labs_memetic_record& d = traces[static_cast<size_t>(r) * s->trace_cap + i];
@@ -1267,22 +771,34 @@ int labs_solver_population(labs_solver* s, uint64_t* words, int32_t* energies) {
 namespace {
 
 struct BlobHeader {
-  uint64_t magic;  // "LABSCKP1"
-  int32_t n, R, K, nw, rng_kind, crossover, replacement, pad_;
+  uint64_t magic;  // "LABSCKP2"
+  int32_t n, R, K, nw;
   int64_t trace_cap;
+  uint64_t base_seed;
+  int64_t replica_offset;
+  // every run parameter that shapes a trajectory (labs_memetic_params)
+  int32_t population_size, rng_kind;
+  double p_comb, p_mutate;
+  int64_t target_energy;
+  double max_seconds;
+  int64_t max_iterations;
+  double min_tabu_factor, max_tabu_factor;
+  int32_t tie_rule, aspiration, crossover, replacement;
 };
-constexpr uint64_t kBlobMagic = 0x31504B4353424C4CULL;
+constexpr uint64_t kBlobMagic = 0x32504B4353424C4CULL;
 
-// (device buffer, bytes) in blob order.
+// (device buffer, bytes) in blob order. Timers are saved as each replica's
+// elapsed run time (s->elapsed, filled by k_elapsed at save), not as raw
+// %globaltimer stamps, so budgets and wall times survive a resume.
 std::vector<std::pair<void*, size_t>> state_parts(labs_solver* s) {
   const size_t R = s->R, K = s->K, nw = s->nw;
   std::vector<std::pair<void*, size_t>> v = {
       {s->pop.p, sizeof(uint64_t) * R * K * nw}, {s->popE.p, sizeof(int32_t) * R * K},
       {s->best.p, sizeof(uint64_t) * R * nw},    {s->bestE.p, sizeof(int32_t) * R},
       {s->iters.p, sizeof(int64_t) * R},         {s->status.p, sizeof(int32_t) * R},
-      {s->init.p, sizeof(int32_t) * R},          {s->tend.p, sizeof(int64_t) * R},
+      {s->init.p, sizeof(int32_t) * R},          {s->elapsed.p, sizeof(int64_t) * R},
       {s->order.p, sizeof(int32_t) * R},         {s->counter.p, sizeof(int32_t)},
-      {s->stop.p, sizeof(int32_t)},              {s->tabu_total.p, sizeof(unsigned long long)},
+      {s->stop, sizeof(int32_t)},                {s->tabu_total.p, sizeof(unsigned long long)},
       {s->tabu_rep.p, sizeof(int64_t) * R}};
   if (s->mt) v.push_back({s->rng.p, sizeof(labs_rng_state) * R});
   else v.push_back({s->ctr.p, sizeof(uint64_t) * R});
@@ -1294,22 +810,55 @@ std::vector<std::pair<void*, size_t>> state_parts(labs_solver* s) {
 }
 
 BlobHeader header_of(labs_solver* s) {
-  BlobHeader h{};
+  BlobHeader h;
+  std::memset(&h, 0, sizeof h);
   h.magic = kBlobMagic;
   h.n = s->n;
   h.R = s->R;
   h.K = s->K;
   h.nw = s->nw;
-  h.rng_kind = s->p.rng_kind;
-  h.crossover = s->p.crossover;
-  h.replacement = s->p.replacement;
   h.trace_cap = s->trace_cap;
+  h.base_seed = s->base_seed;
+  h.replica_offset = s->offset;
+  const labs_memetic_params& p = s->p;
+  h.population_size = p.population_size;
+  h.rng_kind = p.rng_kind;
+  h.p_comb = p.p_comb;
+  h.p_mutate = p.p_mutate;
+  h.target_energy = p.target_energy;
+  h.max_seconds = p.max_seconds;
+  h.max_iterations = p.max_iterations;
+  h.min_tabu_factor = p.tabu.min_tabu_factor;
+  h.max_tabu_factor = p.tabu.max_tabu_factor;
+  h.tie_rule = p.tabu.tie_rule;
+  h.aspiration = p.tabu.aspiration;
+  h.crossover = p.crossover;
+  h.replacement = p.replacement;
   return h;
 }
 
-__global__ void k_restamp(int R, int64_t* t0) {
+// Elapsed run time per replica: finished replicas keep t_end - t0, running
+// ones count up to now; never-initialized replicas have none.
+__global__ void k_elapsed(int R, const int64_t* t0, const int64_t* tend, const int32_t* status,
+                          const int32_t* init, int64_t* elapsed) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < R) t0[r] = globaltimer_ns();
+  if (r >= R) return;
+  if (!init[r]) {
+    elapsed[r] = 0;
+    return;
+  }
+  elapsed[r] = (status[r] != kRunning ? tend[r] : globaltimer_ns()) - t0[r];
+}
+
+// Resume: t0 = now - elapsed, and t_end = now for finished replicas, so
+// t_end - t0 (their wall time) and the max_seconds budget of running ones
+// continue where the checkpoint left them.
+__global__ void k_restamp(int R, const int64_t* elapsed, int64_t* t0, int64_t* tend) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int64_t now = globaltimer_ns();
+  t0[r] = now - elapsed[r];
+  tend[r] = now;
 }
 
 }  // namespace
@@ -1327,6 +876,10 @@ int labs_solver_save(labs_solver* s, void* blob) {
   if (!s || !blob) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
   labs_ctx* ctx = s->ctx;
   LABS_CUDA(cudaSetDevice(ctx->device));
+  k_elapsed<<<(s->R + 127) / 128, 128, 0, ctx->stream>>>(
+      s->R, s->t0.as<int64_t>(), s->tend.as<int64_t>(), s->status.as<int32_t>(),
+      s->init.as<int32_t>(), s->elapsed.as<int64_t>());
+  LABS_CUDA(cudaGetLastError());
   unsigned char* out = static_cast<unsigned char*>(blob);
   const BlobHeader h = header_of(s);
   std::memcpy(out, &h, sizeof h);
@@ -1348,13 +901,17 @@ int labs_solver_load(labs_solver* s, const void* blob) {
   std::memcpy(&h, in, sizeof h);
   const BlobHeader want = header_of(s);
   if (std::memcmp(&h, &want, sizeof h) != 0)
-    return fail(LABS_ERR_INVALID_ARGUMENT, "checkpoint does not match this solver");
+    return fail(LABS_ERR_INVALID_ARGUMENT,
+                "checkpoint does not match this solver (n, replicas, seeds, offset, trace "
+                "capacity and every run parameter must agree)");
   size_t off = sizeof h;
   for (auto& part : state_parts(s)) {
     LABS_H2D(part.first, in + off, part.second);
     off += part.second;
   }
-  k_restamp<<<(s->R + 127) / 128, 128, 0, ctx->stream>>>(s->R, s->t0.as<int64_t>());
+  k_restamp<<<(s->R + 127) / 128, 128, 0, ctx->stream>>>(s->R, s->elapsed.as<int64_t>(),
+                                                          s->t0.as<int64_t>(),
+                                                          s->tend.as<int64_t>());
   LABS_CUDA(cudaGetLastError());
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
   return LABS_OK;
@@ -1418,10 +975,181 @@ int labs_run_replicas(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   return LABS_OK;
 }
 
+int labs_solver_stop_flag(labs_solver* s, int32_t** d_flag) {
+  if (!s || !d_flag) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  *d_flag = s->stop;
+  return LABS_OK;
+}
+
+int labs_solver_set_peer_stops(labs_solver* s, int count, int32_t* const* d_flags) {
+  if (!s || count < 0 || count > LABS_MAX_PEERS || (count && !d_flags))
+    return fail(LABS_ERR_INVALID_ARGUMENT, "peer stop flags: 0..LABS_MAX_PEERS device pointers");
+  for (int i = 0; i < count; ++i)
+    if (!d_flags[i]) return fail(LABS_ERR_INVALID_ARGUMENT, "null peer stop flag");
+  s->A.npeers = count;
+  for (int i = 0; i < kMaxPeerStops; ++i) s->A.peer_stop[i] = i < count ? d_flags[i] : nullptr;
+  return LABS_OK;
+}
+
+int labs_ipc_export(labs_ctx* ctx, const void* d_ptr, void* handle) {
+  if (!ctx || !d_ptr || !handle) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == LABS_IPC_HANDLE_BYTES, "IPC handle size");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  LABS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  std::memcpy(handle, &h, sizeof h);
+  return LABS_OK;
+}
+
+int labs_ipc_open(labs_ctx* ctx, const void* handle, void** d_ptr) {
+  if (!ctx || !handle || !d_ptr) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  LABS_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return LABS_OK;
+}
+
+int labs_ipc_close(labs_ctx* ctx, void* d_ptr) {
+  if (!ctx || !d_ptr) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  LABS_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return LABS_OK;
+}
+
+int labs_run_replicas_multi(labs_ctx* const* ctxs, int ngpu, int n, int replicas,
+                            uint64_t base_seed, const labs_memetic_params* params,
+                            labs_run_result* out, labs_run_result* per_replica,
+                            labs_memetic_record* traces, int64_t trace_cap, int64_t* trace_len) {
+  if (n < 2) return fail(LABS_ERR_INVALID_ARGUMENT, "run needs length >= 2");
+  if (replicas < 1) return fail(LABS_ERR_INVALID_ARGUMENT, "replicas must be >= 1");
+  if (!ctxs || ngpu < 1 || ngpu > LABS_MAX_PEERS + 1)
+    return fail(LABS_ERR_INVALID_ARGUMENT, "need 1..LABS_MAX_PEERS+1 contexts");
+  for (int g = 0; g < ngpu; ++g)
+    if (!ctxs[g]) return fail(LABS_ERR_INVALID_ARGUMENT, "null context");
+  if (int rc = check_memetic(n, params)) return rc;
+  if (!out) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (traces && (trace_cap < 0 || !trace_len))
+    return fail(LABS_ERR_INVALID_ARGUMENT, "traces need a capacity and length outputs");
+  // Contiguous blocks; islands with no replica are dropped.
+  std::vector<int> dev_of, first, count;
+  for (int g = 0, start = 0; g < ngpu; ++g) {
+    const int c = replicas / ngpu + (g < replicas % ngpu ? 1 : 0);
+    if (c > 0) {
+      dev_of.push_back(g);
+      first.push_back(start);
+      count.push_back(c);
+    }
+    start += c;
+  }
+  const int G = static_cast<int>(dev_of.size());
+  // Device-side stop needs peer access between every pair of distinct
+  // devices; a shared publish counter additionally needs native P2P atomics.
+  bool p2p = true, atomics = true;
+  for (int a = 0; a < G; ++a)
+    for (int b = 0; b < G; ++b) {
+      const int da = ctxs[dev_of[a]]->device, db = ctxs[dev_of[b]]->device;
+      if (da == db) continue;
+      int can = 0, nat = 0;
+      LABS_CUDA(cudaDeviceCanAccessPeer(&can, da, db));
+      if (can) LABS_CUDA(cudaDeviceGetP2PAttribute(&nat, cudaDevP2PAttrNativeAtomicSupported, da, db));
+      if (!can) p2p = false;
+      if (!nat) atomics = false;
+      if (can) {
+        LABS_CUDA(cudaSetDevice(da));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else LABS_CUDA(e);
+      }
+    }
+  atomics = atomics && p2p;
+  std::vector<std::unique_ptr<labs_solver, int (*)(labs_solver*)>> sv;
+  for (int i = 0; i < G; ++i) {
+    labs_solver* s = nullptr;
+    if (int rc = labs_solver_create(ctxs[dev_of[i]], n, count[i], base_seed, first[i], params,
+                                    traces ? trace_cap : 0, &s))
+      return rc;
+    sv.emplace_back(s, labs_solver_destroy);
+  }
+  if (p2p && G > 1) {
+    for (int i = 0; i < G; ++i) {
+      int32_t* peers[kMaxPeerStops];
+      int np = 0;
+      for (int j = 0; j < G; ++j)
+        if (j != i) peers[np++] = sv[j]->stop;
+      if (int rc = labs_solver_set_peer_stops(sv[i].get(), np, peers)) return rc;
+      if (atomics) sv[i]->A.pub_counter = sv[0]->counter.as<int32_t>();
+    }
+    // Every solver's initialization (flag and counter memsets) is complete
+    // before any island can raise a peer's flag.
+    for (int i = 0; i < G; ++i) LABS_CUDA(cudaStreamSynchronize(sv[i]->ctx->stream));
+    for (int i = 0; i < G; ++i)
+      if (int rc = labs_solver_run(sv[i].get(), -1, -1.0, 1)) return rc;
+    for (int i = 0; i < G; ++i) {
+      LABS_CUDA(cudaSetDevice(sv[i]->ctx->device));
+      LABS_CUDA(cudaStreamSynchronize(sv[i]->ctx->stream));
+    }
+  } else if (G > 1) {
+    // No peer access: the host forwards the stop between short epochs.
+    for (;;) {
+      for (int i = 0; i < G; ++i)
+        if (int rc = labs_solver_run(sv[i].get(), -1, 0.01, 1)) return rc;
+      int running = 0, stop = 0;
+      for (int i = 0; i < G; ++i) {
+        int32_t run = 0, flag = 0;
+        if (int rc = labs_solver_status(sv[i].get(), &run, nullptr, nullptr)) return rc;
+        LABS_CUDA(cudaMemcpy(&flag, sv[i]->stop, sizeof flag, cudaMemcpyDeviceToHost));
+        running += run;
+        stop |= flag;
+      }
+      if (!running) break;
+      if (stop)
+        for (int i = 0; i < G; ++i)
+          if (int rc = labs_solver_request_stop(sv[i].get())) return rc;
+    }
+  } else {
+    if (int rc = labs_solver_run(sv[0].get(), -1, -1.0, 1)) return rc;
+  }
+  std::vector<labs_run_result> per(replicas);
+  std::vector<int32_t> order(replicas);
+  std::vector<int64_t> rank(replicas);
+  std::vector<labs_memetic_record> tr;
+  std::vector<int64_t> tl;
+  for (int i = 0; i < G; ++i) {
+    const int c = count[i], f = first[i];
+    if (traces) {
+      tr.assign(static_cast<size_t>(c) * trace_cap, labs_memetic_record{});
+      tl.assign(c, 0);
+    }
+    if (int rc = labs_solver_results(sv[i].get(), per.data() + f, traces ? tr.data() : nullptr,
+                                     traces ? tl.data() : nullptr, order.data() + f))
+      return rc;
+    for (int r = 0; r < c; ++r)
+      rank[f + r] = atomics ? order[f + r]
+                            : (static_cast<int64_t>(order[f + r]) << 8) | static_cast<int64_t>(i);
+    if (traces) {
+      std::memcpy(traces + static_cast<size_t>(f) * trace_cap, tr.data(),
+                  sizeof(labs_memetic_record) * tr.size());
+      std::memcpy(trace_len + f, tl.data(), sizeof(int64_t) * c);
+    }
+  }
+  int win = 0;
+  for (int r = 1; r < replicas; ++r)
+    if (per[r].best_energy < per[win].best_energy ||
+        (per[r].best_energy == per[win].best_energy && rank[r] < rank[win]))
+      win = r;
+  *out = per[win];
+  if (per_replica) std::memcpy(per_replica, per.data(), sizeof(labs_run_result) * replicas);
+  return LABS_OK;
+}
+
 }  // extern "C"
 
-extern "C" int labs_bench_int_peak(labs_ctx* ctx, double* gops) {
-  if (!ctx || !gops) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+namespace {
+// Best-of-5 rate of a probe kernel in Gop/s (ops_per_thread_iter lane-ops
+// per thread per loop iteration).
+template <class Kern>
+int probe_rate(labs_ctx* ctx, Kern kern, double ops_per_thread_iter, double* gops) {
   LABS_CUDA(cudaSetDevice(ctx->device));
   DBuf sink;
   LABS_ALLOC(sink, sizeof(int));
@@ -1429,11 +1157,11 @@ extern "C" int labs_bench_int_peak(labs_ctx* ctx, double* gops) {
   cudaEvent_t e0, e1;
   LABS_CUDA(cudaEventCreate(&e0));
   LABS_CUDA(cudaEventCreate(&e1));
-  k_int_peak<<<blocks, threads, 0, ctx->stream>>>(64, 3, sink.as<int>());  // warm-up
+  kern<<<blocks, threads, 0, ctx->stream>>>(64, 3, sink.as<int>());  // warm-up
   float best_ms = 1e30f;
   for (int rep = 0; rep < 5; ++rep) {
     LABS_CUDA(cudaEventRecord(e0, ctx->stream));
-    k_int_peak<<<blocks, threads, 0, ctx->stream>>>(iters, 3 + rep, sink.as<int>());
+    kern<<<blocks, threads, 0, ctx->stream>>>(iters, 3 + rep, sink.as<int>());
     LABS_CUDA(cudaEventRecord(e1, ctx->stream));
     LABS_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
@@ -1443,110 +1171,19 @@ extern "C" int labs_bench_int_peak(labs_ctx* ctx, double* gops) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   LABS_CUDA(cudaGetLastError());
-  const double ops = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+  const double ops = static_cast<double>(blocks) * threads * iters * ops_per_thread_iter;
   *gops = ops / (best_ms * 1e-3) / 1e9;
   return LABS_OK;
 }
-
-// ------------------------------------------------- exhaustive oracle (K5) --
-namespace {
-
-template <class F>
-int dispatch_kmax(int n, F&& f) {
-  if (n <= 16) return f(std::integral_constant<int, 16>{});
-  if (n <= 32) return f(std::integral_constant<int, 32>{});
-  if (n <= 48) return f(std::integral_constant<int, 48>{});
-  return f(std::integral_constant<int, 64>{});
-}
-
-struct ExhaustShape {
-  int B;            // Gray-index bits walked per thread
-  uint64_t blocks;  // threads
-  unsigned grid;
-};
-
-ExhaustShape exhaust_shape(int n) {
-  const int free_bits = n - 1;
-  ExhaustShape sh;
-  sh.B = free_bits > 18 ? free_bits - 18 : 0;  // >= 2^18 threads when possible
-  sh.blocks = 1ULL << (free_bits - sh.B);
-  sh.grid = static_cast<unsigned>((sh.blocks + 127) / 128);
-  return sh;
-}
-
 }  // namespace
 
-extern "C" int labs_exhaustive_optimum(labs_ctx* ctx, int n, int64_t* optimal_energy,
-                                       uint64_t* witnesses, int64_t cap, int64_t* count) {
-  if (!ctx || !optimal_energy || !count || cap < 0 || (cap && !witnesses))
-    return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
-  if (n < 2 || n > 64)
-    return fail(LABS_ERR_INVALID_ARGUMENT, "device exhaustive search needs 2 <= n <= 64");
-  LABS_CUDA(cudaSetDevice(ctx->device));
-  const ExhaustShape sh = exhaust_shape(n);
-  DBuf mins, ids, out, cnt;
-  LABS_ALLOC(mins, sizeof(int) * sh.blocks);
-  LABS_ALLOC(out, sizeof(uint64_t) * std::max<int64_t>(cap, 1));
-  LABS_ALLOC(cnt, sizeof(unsigned long long));
-  LABS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
-  // pass 1: per-block minima
-  int rc = dispatch_kmax(n, [&](auto km) -> int {
-    constexpr int KMAX = decltype(km)::value;
-    k_exhaust_min<KMAX><<<sh.grid, 128, 0, ctx->stream>>>(n, sh.B, sh.blocks, mins.as<int>());
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
-  });
-  if (rc) return rc;
-  std::vector<int> h(sh.blocks);
-  LABS_D2H(h.data(), mins.p, sizeof(int) * sh.blocks);
-  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  const int e = *std::min_element(h.begin(), h.end());
-  std::vector<uint32_t> sel;
-  for (uint64_t t = 0; t < sh.blocks; ++t)
-    if (h[t] == e) sel.push_back(static_cast<uint32_t>(t));
-  // pass 2: witnesses, only in the blocks that hold the optimum
-  LABS_ALLOC(ids, sizeof(uint32_t) * sel.size());
-  LABS_H2D(ids.p, sel.data(), sizeof(uint32_t) * sel.size());
-  rc = dispatch_kmax(n, [&](auto km) -> int {
-    constexpr int KMAX = decltype(km)::value;
-    const int cntb = static_cast<int>(sel.size());
-    k_exhaust_collect<KMAX><<<(cntb + 127) / 128, 128, 0, ctx->stream>>>(
-        n, sh.B, ids.as<uint32_t>(), cntb, e, out.as<uint64_t>(),
-        static_cast<unsigned long long>(cap), cnt.as<unsigned long long>());
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
-  });
-  if (rc) return rc;
-  unsigned long long c = 0;
-  LABS_D2H(&c, cnt.p, sizeof(c));
-  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (cap && c) LABS_D2H(witnesses, out.p, sizeof(uint64_t) * std::min<uint64_t>(c, cap));
-  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  *optimal_energy = e;
-  *count = static_cast<int64_t>(c);
-  return LABS_OK;
+extern "C" int labs_bench_imad_peak(labs_ctx* ctx, double* gmacs) {
+  if (!ctx || !gmacs) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  return probe_rate(ctx, k_imad_peak, 16.0 * 8.0, gmacs);
 }
 
-extern "C" int labs_local_optima(labs_ctx* ctx, int n, int64_t* count) {
-  if (!ctx || !count) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
-  if (n < 2 || n > 64)
-    return fail(LABS_ERR_INVALID_ARGUMENT, "device local-optima census needs 2 <= n <= 64");
-  LABS_CUDA(cudaSetDevice(ctx->device));
-  DBuf cnt;
-  LABS_ALLOC(cnt, sizeof(unsigned long long));
-  LABS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
-  const ExhaustShape sh = exhaust_shape(n);
-  int rc = dispatch_kmax(n, [&](auto km) -> int {
-    constexpr int KMAX = decltype(km)::value;
-    k_local_optima<KMAX><<<sh.grid, 128, 0, ctx->stream>>>(n, sh.B, sh.blocks,
-                                                           cnt.as<unsigned long long>());
-    LABS_CUDA(cudaGetLastError());
-    return LABS_OK;
-  });
-  if (rc) return rc;
-  unsigned long long c = 0;
-  LABS_D2H(&c, cnt.p, sizeof(c));
-  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  *count = 2 * static_cast<int64_t>(c);  // the complement half mirrors every optimum
-  return LABS_OK;
+extern "C" int labs_bench_int_peak(labs_ctx* ctx, double* gops) {
+  if (!ctx || !gops) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  return probe_rate(ctx, k_int_peak, 16.0 * 8.0, gops);
 }
+

@@ -24,6 +24,8 @@
 
 namespace labsk {
 
+constexpr int kMaxPeerStops = LABS_MAX_PEERS;
+
 enum ReplicaStatus : int32_t {
   kRunning = 0,
   kReached = 1,
@@ -61,6 +63,13 @@ struct MemeticArgs {
   labs_rng_state* mt;      // R (MT mode)
   uint64_t* ctr;           // R (Philox mode)
   volatile int32_t* stop;  // device-resident stop flag
+  // Stop flags of the other islands (other GPUs over NVLink P2P, or other
+  // processes' flags opened through CUDA IPC): a replica reaching the target
+  // raises them together with its own, so every GPU sees the stop at its
+  // next loop check without a host round trip (parallel.cpp:40's
+  // request_stop, across devices).
+  int npeers;
+  volatile int32_t* peer_stop[kMaxPeerStops];
   unsigned long long* tabu_iters;  // accumulated tabu iterations (optional)
   int64_t* tabu_per_replica;       // R, tabu iterations per replica
   // optional trace
@@ -263,8 +272,11 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
     ctl.tlen = tlen0 + 1;
     ctl.it = it0 + 1;
     tile_sync<T>();
-    if (A.race && !(static_cast<int64_t>(re < best0 ? re : best0) > A.target) && ln == 0)
+    if (A.race && !(static_cast<int64_t>(re < best0 ? re : best0) > A.target) && ln == 0) {
       *A.stop = 1;  // parallel.cpp:40 — reaching the target raises the flag
+      for (int p = 0; p < A.npeers; ++p) *A.peer_stop[p] = 1;  // other islands
+      if (A.npeers) __threadfence_system();
+    }
   };
 
   // Save the replica's state at the end of its part of this launch.

@@ -45,22 +45,58 @@ class IslandReport:
 
 
 class Islands:
-    """Drive one rank's solver through epochs with cross-rank coordination."""
+    """Drive one rank's solver through epochs with cross-rank coordination.
 
-    def __init__(self, solver, n: int, k_elites: int = 16, device=None, group=None):
+    Device-side stop: with link_stops=True (CUDA solvers, world > 1) every
+    rank exports its solver's stop flag through CUDA IPC and raises the
+    others' flags from the kernel the moment one of its replicas reaches the
+    target (labs_solver_set_peer_stops), so a stop crosses GPUs over NVLink
+    within one memetic iteration instead of waiting for the epoch's host
+    all_reduce. The per-epoch all_reduce remains for the best key and for
+    termination."""
+
+    def __init__(self, solver, n: int, k_elites: int = 16, device=None, group=None,
+                 link_stops: bool = True):
         self.solver, self.n, self.k = solver, n, k_elites
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device if device is not None else torch.device("cpu")
+        # gloo moves host tensors only: stage device buffers through the host
+        backend = dist.get_backend(group) if dist.is_initialized() else None
+        self.stage = self.device.type == "cuda" and backend == "gloo"
+        self.comm_device = torch.device("cpu") if self.stage else self.device
         nw = (n + 63) // 64
         self.el_w = torch.zeros(k_elites * nw, dtype=torch.int64, device=self.device)
         self.el_e = torch.zeros(k_elites, dtype=torch.int64, device=self.device)
         self.all_w = torch.zeros(self.world * k_elites * nw, dtype=torch.int64, device=self.device)
         self.all_e = torch.zeros(self.world * k_elites, dtype=torch.int64, device=self.device)
+        self.peer_ptrs = []
+        if link_stops and self.world > 1 and hasattr(solver, "stop_flag"):
+            self._link_stops()
+
+    def _link_stops(self):
+        ctx = self.solver.ctx
+        mine = ctx.ipc_export(self.solver.stop_flag)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=self.group)
+        self.peer_ptrs = [ctx.ipc_open(h) for r, h in enumerate(handles) if r != self.rank]
+        self.solver.set_peer_stops(self.peer_ptrs)
+        dist.barrier(group=self.group)  # every flag mapped before any kernel runs
+
+    def close(self):
+        """Unlink and unmap the peers' stop flags (before the solver goes)."""
+        if self.peer_ptrs:
+            self.solver.set_peer_stops([])
+            self.solver.sync()
+            if self.world > 1:
+                dist.barrier(group=self.group)  # no peer still raising our flag
+            for p in self.peer_ptrs:
+                self.solver.ctx.ipc_close(p)
+            self.peer_ptrs = []
 
     def _allreduce(self, values, op):
-        t = torch.tensor(values, dtype=torch.int64, device=self.device)
+        t = torch.tensor(values, dtype=torch.int64, device=self.comm_device)
         if self.world > 1:
             dist.all_reduce(t, op=op, group=self.group)
         return t.tolist()
@@ -68,13 +104,23 @@ class Islands:
     def exchange(self, rotation: int):
         """Export top-k, all_gather across ranks, offer to every replica."""
         self.solver.export_elites(self.k, self.el_w.data_ptr(), self.el_e.data_ptr())
-        self.solver.sync()
+        self.solver.sync()  # the export (solver stream) is complete
         if self.world > 1:
-            dist.all_gather_into_tensor(self.all_w, self.el_w, group=self.group)
-            dist.all_gather_into_tensor(self.all_e, self.el_e, group=self.group)
+            src_w = self.el_w.cpu() if self.stage else self.el_w
+            src_e = self.el_e.cpu() if self.stage else self.el_e
+            dst_w = torch.empty(self.all_w.shape, dtype=torch.int64, device=self.comm_device)
+            dst_e = torch.empty(self.all_e.shape, dtype=torch.int64, device=self.comm_device)
+            dist.all_gather_into_tensor(dst_w, src_w, group=self.group)
+            dist.all_gather_into_tensor(dst_e, src_e, group=self.group)
+            self.all_w.copy_(dst_w)
+            self.all_e.copy_(dst_e)
         else:
             self.all_w.copy_(self.el_w)
             self.all_e.copy_(self.el_e)
+        # The gather and copies ran on torch's stream; the import runs on the
+        # solver's own stream, so it must not start before they finish.
+        if self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
         self.solver.import_elites(self.world * self.k, self.all_w.data_ptr(),
                                   self.all_e.data_ptr(), rotation=rotation)
 

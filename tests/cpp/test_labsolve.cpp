@@ -2,7 +2,9 @@
 // headers (proj/include/labsolve/*.hpp) the way its own doctest suites use
 // them (proj/tests/test_{sequence,correlation,tabu,memetic,parallel}.cpp),
 // so the same calls and expectations hold on the B200 implementation.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <set>
@@ -238,6 +240,52 @@ static void parallel() {
   CHECK_THROWS_AS(run_replicas(broken), std::invalid_argument);
 }
 
+// run_replicas over several GPUs (LABS_DEVICES, e.g. "0,0" on a one-GPU box:
+// two islands on one device): every replica's result is the one it has when
+// run alone (seed base_seed + r, parallel.cpp:38), and a target reached on
+// the second island stops the first through the device-side peer flag.
+static void multi_gpu() {
+  MemeticParams params;
+  params.target_energy = 0;
+  params.max_iterations = 7;
+  ParallelConfig cfg;
+  cfg.n = 40;
+  cfg.replicas = 5;  // uneven blocks: 3 + 2
+  cfg.base_seed = 4242;
+  cfg.memetic = params;
+  ReplicaReport report;
+  report.collect_traces = true;
+  RunResult best = run_replicas(cfg, &report);
+  CHECK(report.results.size() == 5);
+  long long lo = 1LL << 40;
+  for (int r = 0; r < 5; ++r) {
+    MemeticTrace tr;
+    RunResult alone = memetic_tabu(40, params, 4242 + r, nullptr, &tr, r);
+    const RunResult& got = report.results[r];
+    CHECK(got.best == alone.best && got.best_energy == alone.best_energy);
+    CHECK(got.iterations == alone.iterations && got.seed == alone.seed);
+    CHECK(got.replica_id == r);
+    CHECK(report.traces[r].iters.size() == tr.iters.size());
+    for (size_t i = 0; i < tr.iters.size() && i < report.traces[r].iters.size(); ++i)
+      CHECK(report.traces[r].iters[i].child_energy == tr.iters[i].child_energy);
+    lo = std::min(lo, alone.best_energy);
+  }
+  CHECK(best.best_energy == lo);
+  // n = 37, target 86: seed 2011 needs 18138 iterations, seed 2012 489
+  // (oracle); with one replica per island the second stops the first.
+  ParallelConfig race;
+  race.n = 37;
+  race.replicas = 2;
+  race.base_seed = 2011;
+  race.memetic.target_energy = 86;
+  race.memetic.max_seconds = 120.0;
+  ReplicaReport rr;
+  RunResult w = run_replicas(race, &rr);
+  CHECK(w.reached_target && w.replica_id == 1 && w.iterations == 489);
+  CHECK(!rr.results[0].reached_target && rr.results[0].iterations < 18138);
+  std::printf("multi-GPU run_replicas over LABS_DEVICES: ok\n");
+}
+
 static std::string g_table = "tests/golden/table2.txt";
 
 static void oracle() {
@@ -269,6 +317,7 @@ int main(int argc, char** argv) {
   tabu();
   memetic();
   parallel();
+  if (std::getenv("LABS_DEVICES")) multi_gpu();
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -1,0 +1,130 @@
+"""The island model with the real device solver at world_size 2 (two processes
+sharing cuda:0, gloo for the host collectives, CUDA IPC for the stop flags).
+
+Checks:
+  * with no stop, every replica of every rank equals the oracle's
+    memetic_tabu(n, base + rank * R + r) (the reference seeding rule,
+    proj/src/parallel.cpp:38) — best, energy, iterations, child trace;
+  * the global best key equals the minimum over ranks;
+  * a target hit on rank 1 stops rank 0 through the device-side peer stop
+    flag (labs_solver_set_peer_stops over an IPC-mapped flag): rank 0's
+    replica needs 18138 iterations to reach E=86 at n=37 (seed 2011, oracle),
+    rank 1's seed 2012 needs 489, so rank 0 must end stopped, unreached, with
+    a trajectory prefix identical to the oracle's.
+The two kernels never wait on one another; they only raise each other's
+flag, so sharing one GPU changes timing, not the outcome."""
+import os
+import socket
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _worker(rank, world, port, mode, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2504_00987_b200 import capi
+        from paper_2504_00987_b200.islands import Islands, unpack_key
+        ctx = capi.Context(0)
+        if mode == "parity":
+            n, R, base = 32, 8, 500
+            params = capi.memetic_params(target_energy=0, max_iterations=6)
+            sv = capi.Solver(ctx, n, R, base_seed=base, replica_offset=rank * R,
+                             params=params, trace_cap=16)
+            isl = Islands(sv, n, k_elites=2, device=torch.device("cuda", 0))
+            rep = isl.run(target=0, epoch_seconds=0.05)
+            res = sv.results()
+            out = {"reps": [(r["replica_id"], r["seed"], r["best_energy"], r["iterations"],
+                             [int(x) for x in r["best"]], [t[2] for t in r["trace"]])
+                            for r in res],
+                   "key": unpack_key(isl.global_best()[0]), "best": rep.best_energy,
+                   "best_replica": rep.best_replica}
+        else:
+            n, R, base, target = 37, 1, 2011, 86
+            params = capi.memetic_params(target_energy=target)
+            sv = capi.Solver(ctx, n, R, base_seed=base, replica_offset=rank * R,
+                             params=params, trace_cap=20000)
+            isl = Islands(sv, n, k_elites=1, device=torch.device("cuda", 0))
+            assert len(isl.peer_ptrs) == 1
+            rep = isl.run(target=target, epoch_seconds=30.0, max_seconds=60.0)
+            r = sv.results()[0]
+            out = {"seed": r["seed"], "best": r["best_energy"], "iterations": r["iterations"],
+                   "reached": r["reached_target"], "trace": [t[2] for t in r["trace"]],
+                   "stop_seen": [t[1] for t in r["trace"]][-1:],
+                   "global_best": rep.best_energy, "global_replica": rep.best_replica,
+                   "epochs": rep.epochs}
+        isl.close()
+        sv.close()
+        q.put((rank, out))
+        dist.destroy_process_group()
+    except Exception as e:  # surface the failure in the parent
+        import traceback
+        q.put((rank, {"error": traceback.format_exc() + repr(e)}))
+
+
+def _run(mode):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in out[r], out[r]["error"]
+    for p in procs:
+        assert p.exitcode == 0
+    return out
+
+
+def test_islands_world2_per_replica_parity():
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    out = _run("parity")
+    R, base = 8, 500
+    keys = []
+    for rank in (0, 1):
+        for r, (rid, seed, e, its, best, trace) in enumerate(out[rank]["reps"]):
+            assert rid == rank * R + r and seed == base + rank * R + r
+            ref = o.memetic(32, seed, child_cap=16, target_energy=0, max_iterations=6)
+            assert (e, its) == (ref["best_energy"], ref["iterations"])
+            assert best == [int(x) for x in ref["best"]]
+            assert trace == ref["child_energies"]
+            keys.append((e, rid))
+    lo = min(keys)
+    for rank in (0, 1):
+        assert out[rank]["best"] == lo[0]
+        assert tuple(out[rank]["key"]) == lo
+        assert out[rank]["best_replica"] == lo[1]
+
+
+def test_islands_world2_target_on_rank1_stops_rank0():
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    out = _run("stop")
+    r0, r1 = out[0], out[1]
+    assert r1["seed"] == 2012 and r1["reached"] and r1["best"] <= 86
+    assert r1["iterations"] == 489  # oracle: memetic_tabu(37, {target 86}, 2012)
+    assert r0["seed"] == 2011 and not r0["reached"]
+    assert r0["iterations"] < 18138  # oracle: seed 2011 needs 18138 iterations
+    assert r0["stop_seen"] == [True]  # the loop-top stop record (memetic.cpp:80-82)
+    ref = o.memetic(37, 2011, child_cap=r0["iterations"], target_energy=86,
+                    max_iterations=r0["iterations"])
+    assert r0["trace"][:-1] == ref["child_energies"][:r0["iterations"]]
+    for r in (r0, r1):
+        assert r["global_best"] == r1["best"] and r["global_replica"] == 1

@@ -139,6 +139,38 @@ def test_checkpoint_resume_is_exact(ctx):
         bad = capi.Solver(ctx, n + 1, R, base_seed=77, params=p, trace_cap=16)
         with pytest.raises(ValueError):
             bad.load(blob)
+        # every trajectory-shaping setting is part of the checkpoint header
+        for kw in ({"base_seed": 78}, {"replica_offset": 5},
+                   {"params": capi.memetic_params(target_energy=3, max_iterations=10,
+                                                  rng_kind=kind)},
+                   {"params": capi.memetic_params(target_energy=0, max_iterations=10,
+                                                  rng_kind=kind, p_comb=0.5)},
+                   {"params": capi.memetic_params(target_energy=0, max_iterations=10,
+                                                  rng_kind=kind, max_tabu_factor=0.2)},
+                   {"params": capi.memetic_params(target_energy=0, max_iterations=11,
+                                                  rng_kind=kind)}):
+            args = {"base_seed": 77, "params": p, "trace_cap": 16, **kw}
+            other = capi.Solver(ctx, n, R, **args)
+            with pytest.raises(ValueError):
+                other.load(blob)
+
+
+def test_checkpoint_keeps_wall_times(ctx):
+    """Finished replicas keep their wall time across save/load, and running
+    ones continue their max_seconds budget (t0 was restamped)."""
+    import time
+    n, R = 40, 8
+    p = capi.memetic_params(target_energy=0, max_iterations=3)
+    a = capi.Solver(ctx, n, R, base_seed=9, params=p)
+    a.run(race=False)
+    before = [r["wall_seconds"] for r in a.results()]
+    blob = a.save()
+    time.sleep(0.3)
+    b = capi.Solver(ctx, n, R, base_seed=9, params=p)
+    b.load(blob)
+    after = [r["wall_seconds"] for r in b.results()]
+    assert all(x > 0 for x in before)
+    assert after == pytest.approx(before, abs=2e-3)
 
 
 def test_islands_driver_single_rank(ctx):
@@ -191,3 +223,39 @@ def test_tile_widths_agree(ctx, monkeypatch, kind, n, asp, tie):
         out[tile] = (_results(sv), sv.population()[1].tolist())
         sv.close()
     assert out["16"] == out["32"]
+
+
+def test_run_replicas_multi_matches_single_gpu(ctx, oracle):
+    """labs_run_replicas_multi over two contexts of one device: contiguous
+    replica blocks (4 + 3), seeds base + r, every replica equal to the oracle
+    and to the single-GPU run; winner = strictly lowest energy."""
+    n, R, base = 36, 7, 321
+    p = capi.memetic_params(target_energy=0, max_iterations=5)
+    ctx2 = capi.Context(0)
+    best, per = capi.run_replicas_multi([ctx, ctx2], n, R, base, p, trace_cap=8)
+    b1, per1 = ctx.run_replicas(n, R, base, p, trace_cap=8)
+    _, ref = oracle.run_replicas(n, R, base, target_energy=0, max_iterations=5)
+    for r in range(R):
+        assert per[r]["replica_id"] == r and per[r]["seed"] == base + r
+        for k in ("best_energy", "iterations", "seed"):
+            assert per[r][k] == per1[r][k] == ref[r][k]
+        assert per[r]["best"].tolist() == per1[r]["best"].tolist() == ref[r]["best"].tolist()
+        assert per[r]["trace"] == per1[r]["trace"]
+    assert best["best_energy"] == min(x["best_energy"] for x in per)
+    one, _ = capi.run_replicas_multi([ctx], n, R, base, p)
+    assert (one["best_energy"], one["replica_id"]) == (b1["best_energy"], b1["replica_id"])
+    with pytest.raises(ValueError):
+        capi.run_replicas_multi([], n, R, base, p)
+    ctx2.close()
+
+
+def test_run_replicas_multi_cross_island_stop(ctx):
+    """A target reached on island 1 stops island 0 through the peer flag:
+    n=37, target 86, seed 2011 needs 18138 iterations and seed 2012 489
+    (oracle), one replica per island."""
+    ctx2 = capi.Context(0)
+    p = capi.memetic_params(target_energy=86, max_seconds=120.0)
+    best, per = capi.run_replicas_multi([ctx, ctx2], 37, 2, 2011, p)
+    assert best["reached_target"] and best["replica_id"] == 1 and best["iterations"] == 489
+    assert not per[0]["reached_target"] and per[0]["iterations"] < 18138
+    ctx2.close()
