@@ -467,7 +467,7 @@ struct labs_solver {
   bool mt = true;
   int64_t trace_cap = 0;
   DBuf pop, popE, best, bestE, iters, status, init, t0, tend, elapsed, order, counter, rng, ctr,
-      tabu_total, tabu_rep, trace, trace_len, taken;
+      tabu_total, tabu_rep, trace, trace_len, taken, peers;
   // The stop flag is a plain cudaMalloc allocation (not stream-ordered) so
   // that other processes can map it through CUDA IPC (labs_ipc_export).
   int32_t* stop = nullptr;
@@ -535,6 +535,7 @@ int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   LABS_ALLOC(s->tabu_total, sizeof(unsigned long long));
   LABS_ALLOC(s->tabu_rep, sizeof(int64_t) * R);
   LABS_ALLOC(s->taken, sizeof(int32_t) * R);
+  LABS_ALLOC(s->peers, sizeof(int32_t*) * kMaxPeerStops);
   if (s->mt) LABS_ALLOC(s->rng, sizeof(labs_rng_state) * R);
   else LABS_ALLOC(s->ctr, sizeof(uint64_t) * R);
   if (trace_cap) {
@@ -591,6 +592,7 @@ int labs_solver_create(labs_ctx* ctx, int n, int replicas, uint64_t base_seed,
   A.ctr = s->mt ? nullptr : s->ctr.as<uint64_t>();
   A.stop = s->stop;
   A.npeers = 0;
+  A.peer_stop = s->peers.as<int32_t*>();
   A.tabu_iters = s->tabu_total.as<unsigned long long>();
   A.tabu_per_replica = s->tabu_rep.as<int64_t>();
   A.trace = trace_cap ? s->trace.as<int64_t>() : nullptr;
@@ -986,8 +988,13 @@ int labs_solver_set_peer_stops(labs_solver* s, int count, int32_t* const* d_flag
     return fail(LABS_ERR_INVALID_ARGUMENT, "peer stop flags: 0..LABS_MAX_PEERS device pointers");
   for (int i = 0; i < count; ++i)
     if (!d_flags[i]) return fail(LABS_ERR_INVALID_ARGUMENT, "null peer stop flag");
+  labs_ctx* ctx = s->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  int32_t* h[kMaxPeerStops] = {};
+  for (int i = 0; i < count; ++i) h[i] = d_flags[i];
+  LABS_H2D(s->peers.p, h, sizeof h);
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
   s->A.npeers = count;
-  for (int i = 0; i < kMaxPeerStops; ++i) s->A.peer_stop[i] = i < count ? d_flags[i] : nullptr;
   return LABS_OK;
 }
 

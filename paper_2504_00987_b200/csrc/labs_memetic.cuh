@@ -69,7 +69,7 @@ struct MemeticArgs {
   // next loop check without a host round trip (parallel.cpp:40's
   // request_stop, across devices).
   int npeers;
-  volatile int32_t* peer_stop[kMaxPeerStops];
+  int32_t* const* peer_stop;  // npeers device pointers (global memory)
   unsigned long long* tabu_iters;  // accumulated tabu iterations (optional)
   int64_t* tabu_per_replica;       // R, tabu iterations per replica
   // optional trace
@@ -102,6 +102,17 @@ template <int T>
 __device__ __forceinline__ bool tile_stop_seen(const volatile int32_t* stop) {
   if constexpr (LABS_BCAST_READS) return __shfl_sync(tile_mask<T>(), *stop, 0, T) != 0;
   else return *stop != 0;
+}
+
+// Reaching the target raises the stop flag (parallel.cpp:40), and the flags
+// of the other islands (peer GPUs over NVLink, or IPC-mapped flags of other
+// processes). Out of line: it runs once per run and must not cost the
+// tabu loop registers.
+static __device__ __noinline__ void raise_stop(volatile int32_t* stop, int32_t* const* peers,
+                                        int npeers) {
+  *stop = 1;
+  for (int p = 0; p < npeers; ++p) *reinterpret_cast<volatile int32_t*>(peers[p]) = 1;
+  if (npeers) __threadfence_system();
 }
 
 // E = sum C_k^2 of a sequence given as chunks (uses scratch C buffer 1's
@@ -272,11 +283,8 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
     ctl.tlen = tlen0 + 1;
     ctl.it = it0 + 1;
     tile_sync<T>();
-    if (A.race && !(static_cast<int64_t>(re < best0 ? re : best0) > A.target) && ln == 0) {
-      *A.stop = 1;  // parallel.cpp:40 — reaching the target raises the flag
-      for (int p = 0; p < A.npeers; ++p) *A.peer_stop[p] = 1;  // other islands
-      if (A.npeers) __threadfence_system();
-    }
+    if (A.race && !(static_cast<int64_t>(re < best0 ? re : best0) > A.target) && ln == 0)
+      raise_stop(A.stop, A.peer_stop, A.npeers);  // parallel.cpp:40
   };
 
   // Save the replica's state at the end of its part of this launch.

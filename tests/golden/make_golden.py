@@ -146,6 +146,9 @@ def main():
     # 6. memetic_tabu (memetic.cpp:44-117).
     memetic = []
     mcases = [dict(n=20, seed=43, target_energy=26)]  # README.md:114-117 (G1)
+    # configs[0] (BASELINE.json): N=32, K=100, run to the optimum E=64 —
+    # survey G4, 793 iterations, best 64C75280
+    mcases.append(dict(n=32, seed=1032, target_energy=64))
     for n in (32, 64, 107, 119):  # survey G3
         mcases.append(dict(n=n, seed=1000 + n, target_energy=0, max_iterations=20))
     for n in (13, 20):  # test_memetic.cpp:106-120
@@ -186,6 +189,10 @@ def main():
                                      max_iterations=its)
         replicas.append({"n": n, "replicas": R, "base_seed": base, "max_iterations": its,
                          "best": best, "per_replica": per})
+    # configs[0] through run_replicas: one replica, seed 1032, target 64 (G4)
+    best, per = ref.run_replicas(32, 1, 1032, threaded=False, target_energy=64)
+    replicas.append({"n": 32, "replicas": 1, "base_seed": 1032, "max_iterations": None,
+                     "target_energy": 64, "best": best, "per_replica": per})
 
     # 8. Exhaustive ground truth (oracle.cpp:70-151): optimal E + canonical
     # witnesses for n = 3..24, strict local-optima census for n = 3..20.

@@ -88,8 +88,10 @@ def test_memetic(golden, oracle):
 
 def test_run_replicas_sequential(golden, oracle):
     for c in golden["replicas"]:
+        its = c["max_iterations"]
         best, per = oracle.run_replicas(c["n"], c["replicas"], c["base_seed"],
-                                        target_energy=0, max_iterations=c["max_iterations"])
+                                        target_energy=c.get("target_energy", 0),
+                                        max_iterations=-1 if its is None else its)
         for a, b in zip(per, c["per_replica"]):
             for k in ("best", "best_energy", "iterations", "seed", "replica_id",
                       "reached_target"):

@@ -177,10 +177,59 @@ def test_readme_trajectory(ctx):
     assert d["reached_target"]
 
 
+def test_configs0_run_to_optimum(ctx, golden):
+    """BASELINE configs[0]: N=32, one population (K=100), fixed seed, run to
+    the known optimum E=64 — survey fingerprint G4 from the compiled
+    reference: reached after 793 iterations with best 64C75280. Checked
+    through labs_memetic (every child energy) and labs_run_replicas."""
+    from paper_2504_00987_b200.sequence import encode_hex
+    g = [m for m in golden["memetic"] if m["n"] == 32 and m["seed"] == 1032][0]
+    assert (g["best_energy"], g["iterations"], g["reached_target"]) == (64, 793, True)
+    d = ctx.memetic(32, 1032, capi.memetic_params(target_energy=64), trace_cap=1000)
+    assert (d["best_energy"], d["iterations"], encode_hex(d["best"], 32)) == (64, 793, "64C75280")
+    assert [t[2] for t in d["trace"]] == g["child_energies"]
+    best, per = ctx.run_replicas(32, 1, 1032, capi.memetic_params(target_energy=64))
+    assert (best["best_energy"], best["iterations"], encode_hex(best["best"], 32)) == \
+        (64, 793, "64C75280")
+    assert best["reached_target"] and best["seed"] == 1032
+
+
+@pytest.mark.parametrize("n", [64, 119])
+def test_bench_scale_replicas_match_oracle(ctx, oracle, n):
+    """The bench configuration itself: R = resident capacity (k_memetic<2,32,MT>
+    at N=64, NS=4 at N=119), run in short time-sliced epochs like bench.py;
+    33 replicas spread over the whole grid (so over every SM's warps)
+    replay the oracle's memetic_tabu(n, base + r) exactly: best, energy,
+    iterations and every child energy."""
+    iters = 4
+    R = capi.Solver.capacity(ctx, n, capi.RNG_MT19937_64)
+    assert R >= 148 * 4
+    p = capi.memetic_params(target_energy=0, max_iterations=iters)
+    sv = capi.Solver(ctx, n, R, base_seed=31337, params=p, trace_cap=iters + 1)
+    launches = 0
+    while True:
+        sv.run(epoch_seconds=0.0005, race=False)
+        launches += 1
+        if sv.status()["running"] == 0:
+            break
+    assert launches > 1  # the epochs really cut the run
+    res = sv.results()
+    picks = sorted(set([k * (R - 1) // 32 for k in range(33)]))
+    for r in picks:
+        want = oracle.memetic(n, 31337 + r, child_cap=iters, target_energy=0,
+                              max_iterations=iters)
+        got = res[r]
+        assert got["seed"] == 31337 + r
+        assert (got["best_energy"], got["iterations"]) == (want["best_energy"], want["iterations"])
+        assert got["best"].tolist() == want["best"]
+        assert [t[2] for t in got["trace"]] == want["child_energies"]
+    sv.close()
+
+
 def test_run_replicas_matches_reference(ctx, golden):
     for c in golden["replicas"]:
         best, per = ctx.run_replicas(c["n"], c["replicas"], c["base_seed"],
-                                     capi.memetic_params(target_energy=0,
+                                     capi.memetic_params(target_energy=c.get("target_energy", 0),
                                                          max_iterations=c["max_iterations"]))
         for a, b in zip(per, c["per_replica"]):
             assert a["best"].tolist() == b["best"]

@@ -239,7 +239,7 @@ def test_run_replicas_multi_matches_single_gpu(ctx, oracle):
         assert per[r]["replica_id"] == r and per[r]["seed"] == base + r
         for k in ("best_energy", "iterations", "seed"):
             assert per[r][k] == per1[r][k] == ref[r][k]
-        assert per[r]["best"].tolist() == per1[r]["best"].tolist() == ref[r]["best"].tolist()
+        assert per[r]["best"].tolist() == per1[r]["best"].tolist() == ref[r]["best"]
         assert per[r]["trace"] == per1[r]["trace"]
     assert best["best_energy"] == min(x["best_energy"] for x in per)
     one, _ = capi.run_replicas_multi([ctx], n, R, base, p)
