@@ -11,6 +11,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "labs_b200.h"
@@ -43,9 +44,15 @@ template <int L, bool MT>
 struct TileSlot {
   uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
   uint64_t out[MT ? kMtN : PhiloxRng::kBlock];  // tempered block / Philox block
+  uint8_t tenure[MT ? kMtN : 4];  // MT: tenure table of the block (labs_rng.cuh)
+  int32_t tenure_par[2];          // MT: its window {min_t, range}
   TileCtl ctl;
   WalkSmemL<L> walk;
 };
+using TileSlotMt64 = TileSlot<64, true>;
+static_assert(offsetof(TileSlotMt64, tenure) - offsetof(TileSlotMt64, out) == kTenOff &&
+                  offsetof(TileSlotMt64, tenure_par) - offsetof(TileSlotMt64, out) == kTenParOff,
+              "the tenure table must follow the tempered block");
 
 template <int L, bool MT>
 __host__ __device__ constexpr size_t tile_slot_bytes() {
@@ -80,6 +87,10 @@ template <int T = 32>
 __device__ __forceinline__ void mt_load(uint64_t* s, uint64_t* out, const labs_rng_state& g,
                                         MtRngT<T>& rng) {
   for (int i = tile_lane<T>(); i < kMtN; i += T) s[i] = g.mt[i];
+  if (tile_lane<T>() == 0) {  // tenure window {0, 1} until a walk sets one
+    reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(out) + kTenParOff)[0] = 0;
+    reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(out) + kTenParOff)[1] = 1;
+  }
   tile_sync<T>();
   mt_temper_all<T>(s, out);
   rng.bind(s, out, g.idx);
@@ -115,7 +126,7 @@ k_build(int n, int count, const uint64_t* __restrict__ words,
       const int j = 32 * b + lane_id();
       if (j < n && nbr) nbr[static_cast<size_t>(item) * n + j] = w.E + dE[b];
       if (j >= 1 && j < n && corr)
-        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.CK[b];
+        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.CK[b] / kCScale;
     }
     if (lane_id() == 0) energy[item] = w.E;
     __syncwarp();

@@ -239,8 +239,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
   ctl.have = 0;
   ctl.ran = 0;
   // walk state (registers)
-  int t = 1, m = 0, min_t = 0, wbestE = 0;
-  uint32_t trange = 1;
+  int t = 1, m = 0, wbestE = 0;
   uint32_t wbest[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) wbest[c] = 0u;
@@ -449,11 +448,11 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
       // tabu_search entry (tabu.cpp:12-29): maxIter, then the tenure window
       // floor(f * m + 1e-9) with two rounded double operations, no FMA.
       m = static_cast<int>(uniform_int(rng, 0, n)) + n / 2;
-      min_t = static_cast<int>(
+      const int min_t = static_cast<int>(
           floor(__dadd_rn(__dmul_rn(A.tabu.min_factor, static_cast<double>(m)), 1e-9)));
       const int max_t = static_cast<int>(
           floor(__dadd_rn(__dmul_rn(A.tabu.max_factor, static_cast<double>(m)), 1e-9)));
-      trange = static_cast<uint32_t>(max_t - min_t + 1);
+      rng.begin_walk(min_t, static_cast<uint32_t>(max_t - min_t + 1));
       w.init(n, child, cb0);
       ctl.ran = 1;
       wbestE = w.E;
@@ -482,7 +481,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
     int pos, dEp, fb, ntie;
     uint32_t msk[NS];
     select_move<NS, T, false>(dE, adm, n, tie_rule, rng, pos, dEp, fb, msk, ntie);
-    const int tenure = min_t + uniform_below(rng, trange);
+    const int tenure = rng.tenure();  // uniform_int(min_t, max_t) (tabu.cpp:49-50)
     w.template apply_cb<decltype(cbc)::value>(pos, dEp, t, tenure);
     if (w.E < wbestE) {
       wbestE = w.E;

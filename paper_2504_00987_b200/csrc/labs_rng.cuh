@@ -120,8 +120,95 @@ __device__ __forceinline__ void sts_u64(uint32_t saddr, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(saddr), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ int32_t lds_s32(uint32_t saddr) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_s32(uint32_t saddr, int32_t v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t saddr) {
+  uint16_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(saddr), "h"(static_cast<uint16_t>(v)) : "memory");
+}
+
+// ------------------------------------------------------- tenure table --
+// The tabu step's tenure draw, uniform_int(min_t, max_t) (tabu.cpp:49-50),
+// is the only RNG draw on every step. In reference-RNG mode its Lemire
+// reduction is precomputed for every draw of the current tempered block:
+// byte i of the table (right after the block) holds min_t + draw_i * range
+// >> 64 for the current walk's window, so a step's draw is one byte load
+// while the engine index still advances by exactly one (the draw order, and
+// so the trajectory, is unchanged). Entries whose reduction might reject
+// (p mod 2^64 < range, probability ~2^-32) hold 0xFF and are never served
+// from the table: tc_hi (the first such index, or the block end) bounds the
+// fast path, and the slow path runs the full uniform_int. The table is
+// rebuilt from the current index when a walk starts (new window) and for
+// the whole block at every twist; windows with max_t > 254 are not cached.
+constexpr uint32_t kTenOff = 8u * kMtN;          // table offset from the block
+constexpr uint32_t kTenParOff = 8u * kMtN + kMtN;  // {min_t, range} (int32 x 2)
+
+// Build table entries [lo, kMtN) from the tempered block; returns the first
+// index >= lo that is not cached (kMtN when all are).
 template <int T>
-__device__ __noinline__ void mt_twist(uint32_t mt, uint32_t out) {
+__device__ __forceinline__ int mt_tenure_fill(uint32_t out, int lo) {
+  const int min_t = lds_s32(out + kTenParOff);
+  const uint32_t r32 = static_cast<uint32_t>(lds_s32(out + kTenParOff + 4));
+  if (min_t + static_cast<int>(r32) - 1 > 254) return lo;
+  int first = kMtN;
+#pragma unroll 1
+  for (int base = lo; base < kMtN; base += T) {
+    const int i = base + tile_lane<T>();
+    bool rej = false;
+    if (i < kMtN) {
+      const uint64_t x = lds_u64(out + 8u * static_cast<uint32_t>(i));
+      const uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+      const uint64_t p1 =
+          static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+      rej = static_cast<uint32_t>(p1) == 0 && static_cast<uint32_t>(p0) < r32;
+      sts_u8(out + kTenOff + i, rej ? 0xFFu : static_cast<uint32_t>(min_t) +
+                                                  static_cast<uint32_t>(p1 >> 32));
+    }
+    const uint32_t b = tile_ballot<T>(rej);
+    if (b && first == kMtN) first = base + __ffs(b) - 1;
+  }
+  tile_sync<T>();
+  return first;
+}
+
+// First index >= lo whose entry is not served from the table.
+template <int T>
+__device__ __noinline__ int mt_tenure_rescan(uint32_t out, int lo) {
+  const int min_t = lds_s32(out + kTenParOff);
+  const int r = lds_s32(out + kTenParOff + 4);
+  if (min_t + r - 1 > 254) return lo;
+#pragma unroll 1
+  for (int base = lo; base < kMtN; base += T) {
+    const int i = base + tile_lane<T>();
+    const uint32_t b = tile_ballot<T>(i < kMtN && lds_u8(out + kTenOff + i) == 0xFFu);
+    if (b) return base + __ffs(b) - 1;
+  }
+  return kMtN;
+}
+
+template <int T>
+__device__ __noinline__ int mt_tenure_table(uint32_t out, int lo, int min_t, uint32_t range) {
+  if (tile_lane<T>() == 0) {
+    sts_s32(out + kTenParOff, min_t);
+    sts_s32(out + kTenParOff + 4, static_cast<int32_t>(range));
+  }
+  tile_sync<T>();
+  return mt_tenure_fill<T>(out, lo);
+}
+
+// Twist, temper the new block, rebuild its tenure table; returns tc_hi.
+template <int T>
+__device__ __noinline__ int mt_twist(uint32_t mt, uint32_t out) {
   const int lane = tile_lane<T>();
   const unsigned tm = tile_mask<T>();
   // i in [0, 156): inputs mt[i], mt[i+1], mt[i+156], all old.
@@ -153,6 +240,7 @@ __device__ __noinline__ void mt_twist(uint32_t mt, uint32_t out) {
   __syncwarp(tm);
   for (int i = lane; i < kMtN; i += T) sts_u64(out + 8 * i, mt_temper(lds_u64(mt + 8 * i)));
   __syncwarp(tm);
+  return mt_tenure_fill<T>(out, 0);
 }
 
 // Temper the current block without advancing (after loading a state).
@@ -163,19 +251,28 @@ __device__ __forceinline__ void mt_temper_all(const uint64_t* mt, uint64_t* out)
 }
 
 template <int T>
+struct MtRngT;
+template <int T>
+struct TenurePick;
+
+template <int T>
 struct MtRngT {
   uint32_t mt_s;   // shared-window address of the raw engine state
-  uint32_t out_s;  // shared-window address of the tempered block
+  uint32_t out_s;  // shared-window address of the tempered block (+ tenure table)
   int idx;         // tile-uniform
+  int tc_hi;       // draws [idx, tc_hi) have their tenure in the table
 
+  // The tempered block must be followed by the tenure table and its
+  // parameters (kTenOff, kTenParOff): see TileSlot (labs_device.cuh).
   __device__ __forceinline__ void bind(uint64_t* raw, uint64_t* tempered, int i) {
     mt_s = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
     out_s = static_cast<uint32_t>(__cvta_generic_to_shared(tempered));
     idx = i;
+    tc_hi = 0;  // no window yet: begin_walk builds it
   }
   __device__ __forceinline__ uint64_t next() {
     if (idx >= kMtN) {
-      mt_twist<T>(mt_s, out_s);
+      tc_hi = mt_twist<T>(mt_s, out_s);
       idx = 0;
     }
     const uint64_t v = lds_u64(out_s + 8u * static_cast<uint32_t>(idx));
@@ -186,11 +283,18 @@ struct MtRngT {
   // with count <= T and not crossing a twist (callers chunk on room()).
   __device__ __forceinline__ int room() {
     if (idx >= kMtN) {
-      mt_twist<T>(mt_s, out_s);
+      tc_hi = mt_twist<T>(mt_s, out_s);
       idx = 0;
     }
     return kMtN - idx;
   }
+  // A walk's tenure window [min_t, min_t + range): tabulate the rest of the
+  // block for it.
+  __device__ __forceinline__ void begin_walk(int min_t, uint32_t range) {
+    tc_hi = mt_tenure_table<T>(out_s, idx < kMtN ? idx : kMtN, min_t, range);
+  }
+  // uniform_int(min_t, min_t + range - 1): one table byte, or the full draw.
+  __device__ __forceinline__ int tenure();
   __device__ __forceinline__ uint64_t peek_lane(int i) const {
     return lds_u64(out_s + 8u * static_cast<uint32_t>(idx + i));
   }
@@ -272,6 +376,13 @@ struct PhiloxRngT {
     // crossing into a new block mid-way is impossible: count <= room()
     ctr = nc;
   }
+  int tmin;        // the walk's tenure window (begin_walk)
+  uint32_t trange;
+  __device__ __forceinline__ void begin_walk(int min_t, uint32_t range) {
+    tmin = min_t;
+    trange = range;
+  }
+  __device__ __forceinline__ int tenure();
 };
 using PhiloxRng = PhiloxRngT<32>;
 
@@ -336,6 +447,28 @@ __device__ __noinline__ DrawTail<R> uniform_below_tail(R rng, uint32_t r32, uint
   return {static_cast<uint32_t>(p1 >> 32), rng};
 }
 
+// Tenure draw outside the table (block end, a possibly-rejecting entry, or
+// an uncached window): the full uniform_int, then the next table bound.
+template <int T>
+struct TenurePick {
+  int v;
+  MtRngT<T> rng;
+};
+template <int T>
+__device__ __noinline__ TenurePick<T> mt_tenure_slow(MtRngT<T> r);
+
+template <int T>
+__device__ __forceinline__ int MtRngT<T>::tenure() {
+  if (idx < tc_hi) {
+    const int v = static_cast<int>(lds_u8(out_s + kTenOff + static_cast<uint32_t>(idx)));
+    ++idx;
+    return v;
+  }
+  const TenurePick<T> p = mt_tenure_slow<T>(*this);
+  *this = p.rng;
+  return p.v;
+}
+
 // uniform_int(0, r - 1) for a known 32-bit range r >= 1: the same Lemire
 // arithmetic (and draw count) as uniform_int, without the range dispatch.
 template <class R>
@@ -350,6 +483,20 @@ __device__ __forceinline__ int uniform_below(R& rng, uint32_t r32) {
     return static_cast<int>(d.v);
   }
   return static_cast<int>(p1 >> 32);
+}
+
+template <int T>
+__device__ __forceinline__ int PhiloxRngT<T>::tenure() {
+  return tmin + uniform_below(*this, trange);
+}
+
+template <int T>
+__device__ __noinline__ TenurePick<T> mt_tenure_slow(MtRngT<T> r) {
+  const int min_t = lds_s32(r.out_s + kTenParOff);
+  const uint32_t range = static_cast<uint32_t>(lds_s32(r.out_s + kTenParOff + 4));
+  const int v = min_t + uniform_below(r, range);
+  r.tc_hi = r.idx < kMtN ? mt_tenure_rescan<T>(r.out_s, r.idx) : kMtN;
+  return {v, r};
 }
 
 template <class R>

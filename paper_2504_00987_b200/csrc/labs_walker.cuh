@@ -62,6 +62,14 @@
 
 namespace labsk {
 
+// Scaled walker state: spins are stored as 16 s (shared memory), C and Q as
+// 8 C / 8 Q (registers and shared memory), so the flip update multiplies by
+// the sign sigma alone (no per-step constant ladder and no x16 shift of
+// s_{2p-j}): D += -sigma (16 s_{2j-p}) + MS ((16 s_{2p-j}) - sigma (2 (8 C)
+// + 8 Q)) - 32 is the update below with every operand as stored.
+constexpr int kSpinScale = 16;
+constexpr int kCScale = 8;
+
 // redux.sync.min over the full warp. The walker's control flow is warp-
 // uniform by construction, so the intrinsic's divergence guard is dead
 // weight on the hot path.
@@ -180,8 +188,8 @@ struct Walker {
       const int bit = ((in[c] & lowmask(n - 32 * c)) >> (((T * b) & 31) + ln)) & 1u;
       const int sp = j < n ? 1 - 2 * bit : 0;
       MS[b] = -sp;
-      s.S[SO + j] = static_cast<int8_t>(sp);
-      if constexpr (Smem::kS4) s.S4[SO + j] = sp;
+      s.S[SO + j] = static_cast<int8_t>(kSpinScale * sp);
+      if constexpr (Smem::kS4) s.S4[SO + j] = kSpinScale * sp;
       EX[b] = j < n ? 0 : INT_MAX;
     }
     const int scratch = cb0 ^ 1;
@@ -217,9 +225,9 @@ struct Walker {
         }
         c = len - 2 * acc;
       }
-      CK[b] = c;
-      s.C2[cb0][L + k] = c;
-      s.C2[cb0][L - k] = c;
+      CK[b] = kCScale * c;
+      s.C2[cb0][L + k] = kCScale * c;
+      s.C2[cb0][L - k] = kCScale * c;
       e2 += c * c;
     }
     E = tile_sum<T>(e2);
@@ -245,14 +253,14 @@ struct Walker {
         }
         qv = (hi - lo + 1) - 2 * acc;
       }
-      s.Q[m] = qv;
+      s.Q[m] = kCScale * qv;
     }
     tile_sync<T>();
     int h[NS], hq[NS];
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = T * b + ln;
-      hq[b] = 4 * (n - 2 + s.Q[2 * j]);
+      hq[b] = 4 * (n - 2) + s.Q[2 * j] * (4 / kCScale);  // 4 (n - 2 + Q_2j)
       h[b] = 0;
     }
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
@@ -261,7 +269,8 @@ struct Walker {
       // (the bit windows are dead by now); spins read as 4-byte windows of
       // S, the backward window byte-reversed.
       int8_t* c8 = reinterpret_cast<int8_t*>(s.C2[scratch]);
-      for (int k = ln; k < L + 4; k += T) c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[cb0][L + k] : 0);
+      for (int k = ln; k < L + 4; k += T)
+        c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[cb0][L + k] / kCScale : 0);
       tile_sync<T>();
       const uint32_t* c8w = reinterpret_cast<const uint32_t*>(c8);
       const uint32_t* s32 = reinterpret_cast<const uint32_t*>(s.S);
@@ -281,19 +290,21 @@ struct Walker {
           acc = __dp4a(cw, fw, acc);
           acc = __dp4a(cw, static_cast<int>(__byte_perm(bw, 0u, 0x0123)), acc);
         }
-        h[b] = acc;
+        h[b] = acc / kSpinScale;  // the spin bytes are scaled
       }
       tile_sync<T>();  // c8 readers done before the scratch buffer is reused
     } else {
 #pragma unroll 2
       for (int k = 1; k < n; ++k) {
-        const int c = s.C2[cb0][L + k];
+        const int c = s.C2[cb0][L + k] / kCScale;
 #pragma unroll
         for (int b = 0; b < NS; ++b) {
           const int j = T * b + ln;
           h[b] += c * (static_cast<int>(s.S[SO + j + k]) + static_cast<int>(s.S[SO + j - k]));
         }
       }
+#pragma unroll
+      for (int b = 0; b < NS; ++b) h[b] /= kSpinScale;
     }
     // Positions j >= n (MS = 0) drift by -32 per step; starting them at
     // 2^22 keeps them positive (never admissible, even under aspiration)
@@ -334,10 +345,11 @@ struct Walker {
     const int ln = tile_lane<T>();
     Smem& s = *sm;
     flush_spin();
-    const auto* sp0 = s.spins();  // int32 (short walkers) or int8 spins
-    const int sig = sp0[SO + pos];
-    // -2 sigma, -4 sigma, -8 sigma, -16 sigma by doubling (no multiplies)
-    const int c2 = -(sig + sig), c4 = c2 + c2, c8 = c4 + c4, c16 = c8 + c8;
+    const auto* sp0 = s.spins();  // int32 (short walkers) or int8 spins, x16
+    const int sig16 = sp0[SO + pos];
+    const int sig = sig16 >> 4;            // old s_p (+1 / -1)
+    const int nsig = -sig;
+    const int c32 = sig * 32;
     const int cbv = CB >= 0 ? CB : cb;
     const int32_t* cgp = &s.C2[cbv][L + ln - pos];
     int32_t* cw = &s.C2[cbv ^ 1][L];
@@ -351,18 +363,19 @@ struct Walker {
     for (int b = 0; b < NS; ++b) {
       const int j = T * b + ln;
       const bool isp = j == pos;
-      const int cg = cgp[T * b];
-      const int qg = qp[T * b];
-      const int s1 = s1p[-T * b];
-      const int s2 = s2p[2 * T * b];
-      const int smv = smp[-T * b];
-      const int spv = spp[T * b];
-      // j != p: D += c16 s_{2j-p} + MS (16 s_{2p-j} + c8 (2 C_{|j-p|} + Q_{p+j})) - 32
-      const int wv = 16 * s1 + c8 * (cg + cg + qg);
-      const int dn = D[b] + c16 * s2 + MS[b] * wv - 32;
+      const int cg = cgp[T * b];    // 8 C_{|j-p|}
+      const int qg = qp[T * b];     // 8 Q_{p+j}
+      const int s1 = s1p[-T * b];   // 16 s_{2p-j}
+      const int s2 = s2p[2 * T * b];  // 16 s_{2j-p}
+      const int smv = smp[-T * b];  // 16 s_{p-j}
+      const int spv = spp[T * b];   // 16 s_{p+j}
+      // j != p: D += -16 sigma s_{2j-p} + MS (16 s_{2p-j} - 8 sigma (2 C_{|j-p|}
+      //          + Q_{p+j})) - 32, with the scaled operands:
+      const int wv = s1 + nsig * (cg + cg + qg);
+      const int dn = D[b] + nsig * s2 + MS[b] * wv - 32;
       D[b] = isp ? -D[b] : dn;       // j == p: dE_p -> -dE_p
-      if (!isp) qp[T * b] = qg - c4 * MS[b];  // Q_{p+j} -= 4 sigma s_j
-      CK[b] += c2 * (smv + spv);       // C_j -= 2 sigma (s_{p-j} + s_{p+j})
+      if (!isp) qp[T * b] = qg + c32 * MS[b];  // Q_{p+j} -= 4 sigma s_j
+      CK[b] += nsig * (smv + spv);     // C_j -= 2 sigma (s_{p-j} + s_{p+j})
       cw[j] = CK[b];
       cw[-j] = CK[b];
       MS[b] = isp ? -MS[b] : MS[b];
@@ -370,7 +383,7 @@ struct Walker {
     }
     cb = cbv ^ 1;
     pend_pos = pos;
-    pend_val = -sig;
+    pend_val = -sig16;
     E += dEp;
     __syncwarp();
   }
