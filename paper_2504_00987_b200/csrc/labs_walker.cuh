@@ -70,6 +70,18 @@ namespace labsk {
 constexpr int kSpinScale = 16;
 constexpr int kCScale = 8;
 
+// Orders one step's shared-memory stores before the next step's loads by
+// other lanes of the (converged) warp. LABS_STEP_FENCE=0 keeps only the
+// compiler barrier: on a converged warp __syncwarp compiles to a NOP behind
+// a divergence check, and a warp's shared-memory accesses execute in order.
+#ifndef LABS_STEP_FENCE
+#define LABS_STEP_FENCE 1
+#endif
+__device__ __forceinline__ void step_fence() {
+  if constexpr (LABS_STEP_FENCE) __syncwarp();
+  else asm volatile("" ::: "memory");
+}
+
 // redux.sync.min over the full warp. The walker's control flow is warp-
 // uniform by construction, so the intrinsic's divergence guard is dead
 // weight on the hot path.
@@ -260,7 +272,7 @@ struct Walker {
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = T * b + ln;
-      hq[b] = 4 * (n - 2) + s.Q[2 * j] * (4 / kCScale);  // 4 (n - 2 + Q_2j)
+      hq[b] = 4 * (n - 2) + s.Q[2 * j] / (kCScale / 4);  // 4 (n - 2 + Q_2j)
       h[b] = 0;
     }
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
@@ -385,7 +397,7 @@ struct Walker {
     pend_pos = pos;
     pend_val = -sig16;
     E += dEp;
-    __syncwarp();
+    step_fence();
   }
 
   // Current sequence as 32-bit chunks (bit 1 = spin -1). Divergence-safe.
