@@ -30,6 +30,9 @@ constexpr int kWarps = 4;  // walkers per block
 #ifndef LABS_MINB_SMALL
 #define LABS_MINB_SMALL 6
 #endif
+#ifndef LABS_MINB_TINY
+#define LABS_MINB_TINY 7
+#endif
 #ifndef LABS_MINB_LARGE
 #define LABS_MINB_LARGE 4
 #endif
@@ -322,7 +325,10 @@ struct PhiloxBind {
 // (labs_memetic.cuh: memetic_tiles).
 template <int NS, int T>
 __host__ __device__ constexpr int min_blocks_memetic() {
-  return T * NS <= 128 ? LABS_MINB_SMALL : LABS_MINB_LARGE;
+  // n <= 64 (one warp per replica): 7 blocks = 28 warps per SM, which the
+  // shared memory allows (7.9 KB per replica) and which caps registers at 72.
+  return T * NS <= 64 && T == 32 ? LABS_MINB_TINY
+                                 : (T * NS <= 128 ? LABS_MINB_SMALL : LABS_MINB_LARGE);
 }
 
 // The two policy switches (aspiration, tie rule) as template parameters, so

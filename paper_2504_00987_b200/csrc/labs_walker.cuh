@@ -42,6 +42,7 @@
 // no-op on the entries valid lanes read.
 #pragma once
 #include <climits>
+#include <cstddef>
 #include <cstdint>
 #include <type_traits>
 
@@ -62,6 +63,42 @@
 
 namespace labsk {
 
+#ifndef LABS_ADDR_ASM
+#define LABS_ADDR_ASM 1
+#endif
+// Compile-time loop: f(std::integral_constant<int, i>) for i in [0, N).
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
+
+// Shared loads/stores at a 32-bit shared-window address plus an immediate.
+template <int OFF>
+__device__ __forceinline__ int lds_s32_off(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ void sts_s32_off(uint32_t a, int v) {
+  asm volatile("st.shared.s32 [%0+%1], %2;" ::"r"(a), "n"(OFF), "r"(v));
+}
+template <int E, int OFF>
+__device__ __forceinline__ int lds_spin(uint32_t a) {
+  int v;
+  if constexpr (E == 4) asm volatile("ld.shared.s32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+  else asm volatile("ld.shared.s8 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int E>
+__device__ __forceinline__ void sts_spin(uint32_t a, int v) {
+  if constexpr (E == 4) asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v));
+  else asm volatile("st.shared.s8 [%0], %1;" ::"r"(a), "r"(v));
+}
+
 // Scaled walker state: spins are stored as 16 s (shared memory), C and Q as
 // 8 C / 8 Q (registers and shared memory), so the flip update multiplies by
 // the sign sigma alone (no per-step constant ladder and no x16 shift of
@@ -75,7 +112,7 @@ constexpr int kCScale = 8;
 // compiler barrier: on a converged warp __syncwarp compiles to a NOP behind
 // a divergence check, and a warp's shared-memory accesses execute in order.
 #ifndef LABS_STEP_FENCE
-#define LABS_STEP_FENCE 1
+#define LABS_STEP_FENCE 0
 #endif
 __device__ __forceinline__ void step_fence() {
   if constexpr (LABS_STEP_FENCE) __syncwarp();
@@ -185,6 +222,16 @@ struct Walker {
   int cb;        // C2 buffer holding the current C
   int pend_pos;  // flipped position whose spin store is pending (-1: none)
   int pend_val;
+#if LABS_ADDR_ASM
+  // Shared-window byte addresses of the step's gathers, lane constants set by
+  // init (e = spin element size): aS0 = &spins[SO], aLm = aS0 - e ln,
+  // aLp = aS0 + e ln, aL2 = aS0 + 2 e ln; for byte spins also the C mirror
+  // and Q bases (for int32 spins those are aLp / aLm plus an immediate).
+  // A step then forms each gather address with one IMAD of the flipped
+  // position, and every slot offset is an immediate.
+  uint32_t aS0, aLm, aLp, aL2, aCp, aCm, aQ;
+  uint32_t pend_a;  // address of the pending spin store
+#endif
 
   // Build C, Q, h, E from `in` (chunks of 32 positions, padding zero) with C
   // in buffer cb0 (the other buffer is scratch until the first step).
@@ -246,6 +293,21 @@ struct Walker {
     cb = cb0;
     pend_pos = -1;
     pend_val = 0;
+#if LABS_ADDR_ASM
+    {
+      constexpr uint32_t e = sizeof(*s.spins());
+      const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(&s));
+      aS0 = base + static_cast<uint32_t>(reinterpret_cast<const char*>(s.spins() + SO) -
+                                         reinterpret_cast<const char*>(&s));
+      aLm = aS0 - e * ln;
+      aLp = aS0 + e * ln;
+      aL2 = aS0 + 2 * e * ln;
+      aCp = base + 4u * (L + ln);
+      aCm = base + 4u * (L - ln);
+      aQ = base + static_cast<uint32_t>(offsetof(Smem, Q)) + 4u * ln;
+      pend_a = aS0 - e;  // padding entry: the first flush rewrites its zero
+    }
+#endif
     // Q_m = sum_i s_i s_{m-i}: s against reversed s at offset n-1-m.
 #pragma unroll 1
     for (int a = 0; a < 2 * NS; ++a) {
@@ -354,6 +416,12 @@ struct Walker {
   // index from `cb` (one step body, smaller code).
   template <int CB>
   __device__ __forceinline__ void apply_cb(int pos, int dEp, int t, int tenure) {
+#if LABS_ADDR_ASM
+    if constexpr (CB >= 0) {
+      apply_asm<CB>(pos, dEp, t, tenure);
+      return;
+    }
+#endif
     const int ln = tile_lane<T>();
     Smem& s = *sm;
     flush_spin();
@@ -399,6 +467,78 @@ struct Walker {
     E += dEp;
     step_fence();
   }
+
+#if LABS_ADDR_ASM
+  // Per-step operands of apply_asm's slot updates.
+  struct StepOps {
+    uint32_t a1, a2, a3, a4, a5, a6, aW, aWm;
+    int pos, ln, nsig, c32, exp_new;
+  };
+  template <int CB, int B>
+  __device__ __forceinline__ void slot_asm(const StepOps& o) {
+    using SE = std::remove_pointer_t<decltype(sm->spins())>;
+    constexpr int e = sizeof(SE);
+    constexpr bool kS4 = e == 4;
+    constexpr int kBufC = CB * 8 * L, kBufW = (CB ^ 1) * 8 * L;
+    constexpr int kC = kS4 ? 4 * L - (int)offsetof(Smem, S4) - 4 * SO : 0;
+    constexpr int kQ = kS4 ? (int)offsetof(Smem, Q) - (int)offsetof(Smem, S4) - 4 * SO : 0;
+    const int j = T * B + o.ln;
+    const bool isp = j == o.pos;
+    const int cg = lds_s32_off<kBufC + kC + 4 * T * B>(o.a5);   // 8 C_{|j-p|}
+    const int qg = lds_s32_off<kQ + 4 * T * B>(o.a6);           // 8 Q_{p+j}
+    const int s1 = lds_spin<e, -e * T * B>(o.a1);               // 16 s_{2p-j}
+    const int s2 = lds_spin<e, 2 * e * T * B>(o.a4);            // 16 s_{2j-p}
+    const int smv = lds_spin<e, -e * T * B>(o.a2);              // 16 s_{p-j}
+    const int spv = lds_spin<e, e * T * B>(o.a3);               // 16 s_{p+j}
+    const int wv = s1 + o.nsig * (cg + cg + qg);
+    const int dn = D[B] + o.nsig * s2 + MS[B] * wv - 32;
+    D[B] = isp ? -D[B] : dn;
+    if (!isp) sts_s32_off<kQ + 4 * T * B>(o.a6, qg + o.c32 * MS[B]);
+    CK[B] += o.nsig * (smv + spv);
+    sts_s32_off<kBufW + kC + 4 * T * B>(o.aW, CK[B]);
+    sts_s32_off<kBufW + kC - 4 * T * B>(o.aWm, CK[B]);
+    MS[B] = isp ? -MS[B] : MS[B];
+    EX[B] = isp ? o.exp_new : EX[B];
+    if constexpr (B + 1 < NS) slot_asm<CB, B + 1>(o);
+  }
+
+  // apply_cb with explicit shared-window addressing: one IMAD per gather
+  // base per step, every slot offset and buffer choice an immediate.
+  template <int CB>
+  __device__ __forceinline__ void apply_asm(int pos, int dEp, int t, int tenure) {
+    using SE = std::remove_pointer_t<decltype(sm->spins())>;
+    constexpr int e = sizeof(SE);
+    constexpr bool kS4 = e == 4;
+    sts_spin<e>(pend_a, pend_val);  // the previous flip's spin
+    const uint32_t up = static_cast<uint32_t>(pos);
+    const uint32_t a_sig = aS0 + e * up;
+    const int sig16 = lds_spin<e, 0>(a_sig);
+    const int sig = sig16 >> 4;
+    StepOps o;
+    o.nsig = -sig;
+    o.c32 = sig * 32;
+    o.pos = pos;
+    o.ln = tile_lane<T>();
+    o.exp_new = t + tenure;
+    o.a1 = aLm + 2 * e * up;  // s_{2p-j}
+    o.a2 = aLm + e * up;      // s_{p-j}
+    o.a3 = aLp + e * up;      // s_{p+j}
+    o.a4 = aL2 - e * up;      // s_{2j-p}
+    // C_{|j-p|} at C2[CB][L + j - p]; Q_{p+j}; C stores at C2[CB^1][L +- j]
+    // (for int32 spins the C and Q bases are the spin lanes + immediates)
+    o.a5 = (kS4 ? aLp : aCp) - 4 * up;
+    o.a6 = kS4 ? o.a3 : aQ + 4 * up;
+    o.aW = kS4 ? aLp : aCp;
+    o.aWm = kS4 ? aLm : aCm;
+    slot_asm<CB, 0>(o);
+    cb = CB ^ 1;
+    pend_pos = pos;
+    pend_a = a_sig;
+    pend_val = -sig16;
+    E += dEp;
+    step_fence();
+  }
+#endif
 
   // Current sequence as 32-bit chunks (bit 1 = spin -1). Divergence-safe.
   __device__ __forceinline__ void chunks(uint32_t (&out)[NC]) const {
