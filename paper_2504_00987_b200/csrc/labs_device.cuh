@@ -129,7 +129,7 @@ k_build(int n, int count, const uint64_t* __restrict__ words,
       const int j = 32 * b + lane_id();
       if (j < n && nbr) nbr[static_cast<size_t>(item) * n + j] = w.E + dE[b];
       if (j >= 1 && j < n && corr)
-        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.CK[b] / kCScale;
+        corr[static_cast<size_t>(item) * (n - 1) + j - 1] = w.CK[b] / Walker<NS>::Sc::kC;
     }
     if (lane_id() == 0) energy[item] = w.E;
     __syncwarp();

@@ -21,6 +21,14 @@
 #pragma once
 #include <cstdint>
 
+// Rare selection / draw paths of the tabu step (tie draw, fallback move,
+// tenure outside the table) inline as cold blocks instead of out-of-line
+// calls: no call-ABI register shuffling on the hot path, at the price of a
+// larger loop body.
+#ifndef LABS_RARE_INLINE
+#define LABS_RARE_INLINE 0
+#endif
+
 namespace labsk {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -464,9 +472,17 @@ __device__ __forceinline__ int MtRngT<T>::tenure() {
     ++idx;
     return v;
   }
+#if LABS_RARE_INLINE
+  const int min_t = lds_s32(out_s + kTenParOff);
+  const uint32_t range = static_cast<uint32_t>(lds_s32(out_s + kTenParOff + 4));
+  const int v = min_t + uniform_below(*this, range);
+  tc_hi = idx < kMtN ? mt_tenure_rescan<T>(out_s, idx) : kMtN;
+  return v;
+#else
   const TenurePick<T> p = mt_tenure_slow<T>(*this);
   *this = p.rng;
   return p.v;
+#endif
 }
 
 // uniform_int(0, r - 1) for a known 32-bit range r >= 1: the same Lemire

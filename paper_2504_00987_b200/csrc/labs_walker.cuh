@@ -54,11 +54,16 @@
 #ifndef LABS_TIE_INLINE
 #define LABS_TIE_INLINE 0
 #endif
+
 #ifndef LABS_TIE_XOR
 #define LABS_TIE_XOR 1
 #endif
+
 #ifndef LABS_S4_MAX_L
 #define LABS_S4_MAX_L 64
+#endif
+#ifndef LABS_SINGLE_C
+#define LABS_SINGLE_C 1
 #endif
 
 namespace labsk {
@@ -104,8 +109,21 @@ __device__ __forceinline__ void sts_spin(uint32_t a, int v) {
 // the sign sigma alone (no per-step constant ladder and no x16 shift of
 // s_{2p-j}): D += -sigma (16 s_{2j-p}) + MS ((16 s_{2p-j}) - sigma (2 (8 C)
 // + 8 Q)) - 32 is the update below with every operand as stored.
-constexpr int kSpinScale = 16;
-constexpr int kCScale = 8;
+//
+// For walkers of L <= LABS_S4_MAX_L (int32 spins) the scales grow by 256 so
+// that D itself is the argmin key: D = 256 dE_j + j (keyed), spins 4096 s,
+// C and Q 2048 C / 2048 Q. The selection then needs no per-slot key build,
+// and the flipped slot becomes 2p - D.
+template <int L>
+struct WalkScales {
+  static constexpr bool kKeyed = L <= LABS_S4_MAX_L;  // D carries the key
+  static constexpr int kD = kKeyed ? 256 : 1;        // D = kD dE (+ j)
+  static constexpr int kSpin = 16 * kD;              // step spins (S4 / S)
+  static constexpr int kSpinShift = kKeyed ? 12 : 4;
+  static constexpr int kS8 = kKeyed ? 1 : 16;        // the int8 spin array
+  static constexpr int kC = 8 * kD;                  // C and Q
+  static_assert(kSpin == 2 * kC, "the Q update uses 2 x the stored spin of p");
+};
 
 // Orders one step's shared-memory stores before the next step's loads by
 // other lanes of the (converged) warp. LABS_STEP_FENCE=0 keeps only the
@@ -135,7 +153,12 @@ struct WalkSmemL {
   static constexpr int L = L_;
   static_assert(L % 32 == 0, "walker length must be a multiple of 32 positions");
   static constexpr int NC = L / 32;  // 32-bit chunks of a sequence
-  int32_t C2[2][2 * L];        // C2[buf][L + d] = C_{|d|}, d in (-L, L); 2 buffers
+  // C mirror, C2[buf][L + d] = C_{|d|} for d in (-L, L). LABS_SINGLE_C: one
+  // buffer — a step issues every gather before any store, and the warp's
+  // shared accesses execute in order, so the stores never reach a gather of
+  // the same step; else two buffers (a step reads one, writes the other).
+  static constexpr int kCBuf = LABS_SINGLE_C ? 1 : 2;
+  int32_t C2[kCBuf][2 * L];
   int32_t Q[2 * L];            // Q[m], m in [0, 2n-1)
   static constexpr int SO = L + 4;  // spin x lives at S[SO + x] and S4[SO + x]
   int8_t S[3 * L + 8];         // spins (+1/-1); 0 outside [0, n) (4 guard bytes)
@@ -149,12 +172,20 @@ struct WalkSmemL {
     if constexpr (kS4) return S4;
     else return S;
   }
-  // Packed bit windows for the O(n^2/32) popcount build, aliased onto the C
-  // buffer that is idle until the walk's first step: B32 holds s (position
-  // x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
+  // Packed bit windows for the O(n^2/32) popcount build: B32 holds s
+  // (position x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
+  // With two C buffers they alias the buffer that is idle until the walk's
+  // first step; with one they (and the h build's int8 C) use W.
   static constexpr int kBitWords = 3 * NC + 2;
   static_assert(2 * kBitWords <= 2 * L, "bit windows must fit one C buffer");
-  __device__ __forceinline__ uint32_t* B32(int buf) { return reinterpret_cast<uint32_t*>(C2[buf]); }
+  static constexpr int kScratchWords =
+      LABS_SINGLE_C ? (2 * kBitWords > (L + 4 + 3) / 4 ? 2 * kBitWords : (L + 4 + 3) / 4) : 1;
+  uint32_t W[kScratchWords];
+  __device__ __forceinline__ uint32_t* scratch(int buf) {
+    if constexpr (LABS_SINGLE_C) return W;
+    else return reinterpret_cast<uint32_t*>(C2[buf]);
+  }
+  __device__ __forceinline__ uint32_t* B32(int buf) { return scratch(buf); }
   __device__ __forceinline__ uint32_t* R32(int buf) { return B32(buf) + kBitWords; }
   // Zero both windows of buffer `buf` and store the payload chunks of s.
   template <int T>
@@ -213,6 +244,8 @@ template <int NS, int T = 32>
 struct Walker {
   static constexpr int L = T * NS;
   using Smem = WalkSmemL<L>;
+  using Sc = WalkScales<L>;
+  static constexpr bool kKeyed = Sc::kKeyed;
   static constexpr int NC = Smem::NC;
   static constexpr int SO = Smem::SO;
   Smem* sm;
@@ -247,11 +280,12 @@ struct Walker {
       const int bit = ((in[c] & lowmask(n - 32 * c)) >> (((T * b) & 31) + ln)) & 1u;
       const int sp = j < n ? 1 - 2 * bit : 0;
       MS[b] = -sp;
-      s.S[SO + j] = static_cast<int8_t>(kSpinScale * sp);
-      if constexpr (Smem::kS4) s.S4[SO + j] = kSpinScale * sp;
+      s.S[SO + j] = static_cast<int8_t>(Sc::kS8 * sp);
+      if constexpr (Smem::kS4) s.S4[SO + j] = Sc::kSpin * sp;
       EX[b] = j < n ? 0 : INT_MAX;
     }
     const int scratch = cb0 ^ 1;
+    if constexpr (LABS_SINGLE_C) cb0 = 0;  // one C buffer; scratch is W
     s.template put_bits<T>(n, in, scratch);
     uint32_t* B32 = s.B32(scratch);
     uint32_t* R32 = s.R32(scratch);
@@ -284,9 +318,9 @@ struct Walker {
         }
         c = len - 2 * acc;
       }
-      CK[b] = kCScale * c;
-      s.C2[cb0][L + k] = kCScale * c;
-      s.C2[cb0][L - k] = kCScale * c;
+      CK[b] = Sc::kC * c;
+      s.C2[cb0][L + k] = Sc::kC * c;
+      s.C2[cb0][L - k] = Sc::kC * c;
       e2 += c * c;
     }
     E = tile_sum<T>(e2);
@@ -327,14 +361,14 @@ struct Walker {
         }
         qv = (hi - lo + 1) - 2 * acc;
       }
-      s.Q[m] = kCScale * qv;
+      s.Q[m] = Sc::kC * qv;
     }
     tile_sync<T>();
     int h[NS], hq[NS];
 #pragma unroll
     for (int b = 0; b < NS; ++b) {
       const int j = T * b + ln;
-      hq[b] = 4 * (n - 2) + s.Q[2 * j] / (kCScale / 4);  // 4 (n - 2 + Q_2j)
+      hq[b] = 4 * (n - 2) + s.Q[2 * j] / (Sc::kC / 4);  // 4 (n - 2 + Q_2j)
       h[b] = 0;
     }
     // h_j = sum_k C_k (s_{j+k} + s_{j-k}).
@@ -342,9 +376,9 @@ struct Walker {
       // |C_k| <= 127: four lags per DP4A. C as int8 in the scratch C buffer
       // (the bit windows are dead by now); spins read as 4-byte windows of
       // S, the backward window byte-reversed.
-      int8_t* c8 = reinterpret_cast<int8_t*>(s.C2[scratch]);
+      int8_t* c8 = reinterpret_cast<int8_t*>(s.scratch(scratch));
       for (int k = ln; k < L + 4; k += T)
-        c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[cb0][L + k] / kCScale : 0);
+        c8[k] = static_cast<int8_t>(k >= 1 && k < n ? s.C2[cb0][L + k] / Sc::kC : 0);
       tile_sync<T>();
       const uint32_t* c8w = reinterpret_cast<const uint32_t*>(c8);
       const uint32_t* s32 = reinterpret_cast<const uint32_t*>(s.S);
@@ -364,13 +398,13 @@ struct Walker {
           acc = __dp4a(cw, fw, acc);
           acc = __dp4a(cw, static_cast<int>(__byte_perm(bw, 0u, 0x0123)), acc);
         }
-        h[b] = acc / kSpinScale;  // the spin bytes are scaled
+        h[b] = acc / Sc::kS8;  // the spin bytes are scaled
       }
       tile_sync<T>();  // c8 readers done before the scratch buffer is reused
     } else {
 #pragma unroll 2
       for (int k = 1; k < n; ++k) {
-        const int c = s.C2[cb0][L + k] / kCScale;
+        const int c = s.C2[cb0][L + k] / Sc::kC;
 #pragma unroll
         for (int b = 0; b < NS; ++b) {
           const int j = T * b + ln;
@@ -378,19 +412,29 @@ struct Walker {
         }
       }
 #pragma unroll
-      for (int b = 0; b < NS; ++b) h[b] /= kSpinScale;
+      for (int b = 0; b < NS; ++b) h[b] /= Sc::kS8;
     }
     // Positions j >= n (MS = 0) drift by -32 per step; starting them at
     // 2^22 keeps them positive (never admissible, even under aspiration)
     // for > 10^5 steps, far beyond any walk.
 #pragma unroll
-    for (int b = 0; b < NS; ++b) D[b] = T * b + ln < n ? hq[b] + MS[b] * 4 * h[b] : (1 << 22);
+    for (int b = 0; b < NS; ++b) {
+      const int j = T * b + ln;
+      D[b] = (j < n ? hq[b] + MS[b] * 4 * h[b] : (1 << 22)) * Sc::kD + (Sc::kKeyed ? j : 0);
+    }
+  }
+
+  // The selection's operand for every slot: the argmin key 256 dE_j + j
+  // when keyed, else dE_j.
+  __device__ __forceinline__ void raw(int (&d)[NS]) const {
+#pragma unroll
+    for (int b = 0; b < NS; ++b) d[b] = D[b];
   }
 
   // dE_j for every slot.
   __device__ __forceinline__ void delta(int (&dE)[NS]) const {
 #pragma unroll
-    for (int b = 0; b < NS; ++b) dE[b] = D[b];
+    for (int b = 0; b < NS; ++b) dE[b] = Sc::kKeyed ? D[b] >> 8 : D[b];
   }
 
   // Spin store of the previous flip, performed by every lane before it reads
@@ -417,19 +461,21 @@ struct Walker {
   template <int CB>
   __device__ __forceinline__ void apply_cb(int pos, int dEp, int t, int tenure) {
 #if LABS_ADDR_ASM
-    if constexpr (CB >= 0) {
-      apply_asm<CB>(pos, dEp, t, tenure);
+    if constexpr (LABS_SINGLE_C || CB >= 0) {
+      apply_asm<LABS_SINGLE_C ? 0 : CB>(pos, dEp, t, tenure);
       return;
     }
+#else
+    static_assert(!LABS_SINGLE_C, "the single C buffer needs the ordered (asm) update");
 #endif
     const int ln = tile_lane<T>();
     Smem& s = *sm;
     flush_spin();
     const auto* sp0 = s.spins();  // int32 (short walkers) or int8 spins, x16
     const int sig16 = sp0[SO + pos];
-    const int sig = sig16 >> 4;            // old s_p (+1 / -1)
+    const int sig = sig16 >> Sc::kSpinShift;  // old s_p (+1 / -1)
     const int nsig = -sig;
-    const int c32 = sig * 32;
+    const int c32 = sig16 + sig16;  // 4 kC sigma (kSpin = 2 kC)
     const int cbv = CB >= 0 ? CB : cb;
     const int32_t* cgp = &s.C2[cbv][L + ln - pos];
     int32_t* cw = &s.C2[cbv ^ 1][L];
@@ -452,8 +498,8 @@ struct Walker {
       // j != p: D += -16 sigma s_{2j-p} + MS (16 s_{2p-j} - 8 sigma (2 C_{|j-p|}
       //          + Q_{p+j})) - 32, with the scaled operands:
       const int wv = s1 + nsig * (cg + cg + qg);
-      const int dn = D[b] + nsig * s2 + MS[b] * wv - 32;
-      D[b] = isp ? -D[b] : dn;       // j == p: dE_p -> -dE_p
+      const int dn = D[b] + nsig * s2 + MS[b] * wv - 32 * Sc::kD;
+      D[b] = isp ? (Sc::kKeyed ? 2 * pos - D[b] : -D[b]) : dn;  // j == p: dE_p -> -dE_p
       if (!isp) qp[T * b] = qg + c32 * MS[b];  // Q_{p+j} -= 4 sigma s_j
       CK[b] += nsig * (smv + spv);     // C_j -= 2 sigma (s_{p-j} + s_{p+j})
       cw[j] = CK[b];
@@ -474,49 +520,60 @@ struct Walker {
     uint32_t a1, a2, a3, a4, a5, a6, aW, aWm;
     int pos, ln, nsig, c32, exp_new;
   };
+  // A slot's six gathers (pre-flip values).
+  struct SlotIn {
+    int cg, qg, s1, s2, smv, spv;
+  };
+  template <int CB>
+  static constexpr int kBufC = LABS_SINGLE_C ? 0 : CB * 8 * L;
+  template <int CB>
+  static constexpr int kBufW = LABS_SINGLE_C ? 0 : (CB ^ 1) * 8 * L;
+  using SpinT = std::remove_pointer_t<decltype(static_cast<Smem*>(nullptr)->spins())>;
+  static constexpr int kE = sizeof(SpinT);
+  static constexpr bool kS4 = kE == 4;
+  static constexpr int kCOff = kS4 ? 4 * L - (int)offsetof(Smem, S4) - 4 * SO : 0;
+  static constexpr int kQOff = kS4 ? (int)offsetof(Smem, Q) - (int)offsetof(Smem, S4) - 4 * SO : 0;
+
   template <int CB, int B>
-  __device__ __forceinline__ void slot_asm(const StepOps& o) {
-    using SE = std::remove_pointer_t<decltype(sm->spins())>;
-    constexpr int e = sizeof(SE);
-    constexpr bool kS4 = e == 4;
-    constexpr int kBufC = CB * 8 * L, kBufW = (CB ^ 1) * 8 * L;
-    constexpr int kC = kS4 ? 4 * L - (int)offsetof(Smem, S4) - 4 * SO : 0;
-    constexpr int kQ = kS4 ? (int)offsetof(Smem, Q) - (int)offsetof(Smem, S4) - 4 * SO : 0;
+  __device__ __forceinline__ void slot_load(const StepOps& o, SlotIn (&v)[NS]) {
+    constexpr int e = kE;
+    v[B].cg = lds_s32_off<kBufC<CB> + kCOff + 4 * T * B>(o.a5);  // kC C_{|j-p|}
+    v[B].qg = lds_s32_off<kQOff + 4 * T * B>(o.a6);              // kC Q_{p+j}
+    v[B].s1 = lds_spin<e, -e * T * B>(o.a1);                     // kSpin s_{2p-j}
+    v[B].s2 = lds_spin<e, 2 * e * T * B>(o.a4);                  // kSpin s_{2j-p}
+    v[B].smv = lds_spin<e, -e * T * B>(o.a2);                    // kSpin s_{p-j}
+    v[B].spv = lds_spin<e, e * T * B>(o.a3);                     // kSpin s_{p+j}
+    if constexpr (B + 1 < NS) slot_load<CB, B + 1>(o, v);
+  }
+  template <int CB, int B>
+  __device__ __forceinline__ void slot_store(const StepOps& o, const SlotIn (&v)[NS]) {
     const int j = T * B + o.ln;
     const bool isp = j == o.pos;
-    const int cg = lds_s32_off<kBufC + kC + 4 * T * B>(o.a5);   // 8 C_{|j-p|}
-    const int qg = lds_s32_off<kQ + 4 * T * B>(o.a6);           // 8 Q_{p+j}
-    const int s1 = lds_spin<e, -e * T * B>(o.a1);               // 16 s_{2p-j}
-    const int s2 = lds_spin<e, 2 * e * T * B>(o.a4);            // 16 s_{2j-p}
-    const int smv = lds_spin<e, -e * T * B>(o.a2);              // 16 s_{p-j}
-    const int spv = lds_spin<e, e * T * B>(o.a3);               // 16 s_{p+j}
-    const int wv = s1 + o.nsig * (cg + cg + qg);
-    const int dn = D[B] + o.nsig * s2 + MS[B] * wv - 32;
-    D[B] = isp ? -D[B] : dn;
-    if (!isp) sts_s32_off<kQ + 4 * T * B>(o.a6, qg + o.c32 * MS[B]);
-    CK[B] += o.nsig * (smv + spv);
-    sts_s32_off<kBufW + kC + 4 * T * B>(o.aW, CK[B]);
-    sts_s32_off<kBufW + kC - 4 * T * B>(o.aWm, CK[B]);
+    const int wv = v[B].s1 + o.nsig * (v[B].cg + v[B].cg + v[B].qg);
+    const int dn = D[B] + o.nsig * v[B].s2 + MS[B] * wv - 32 * Sc::kD;
+    D[B] = isp ? (Sc::kKeyed ? 2 * o.pos - D[B] : -D[B]) : dn;
+    if (!isp) sts_s32_off<kQOff + 4 * T * B>(o.a6, v[B].qg + o.c32 * MS[B]);
+    CK[B] += o.nsig * (v[B].smv + v[B].spv);
+    sts_s32_off<kBufW<CB> + kCOff + 4 * T * B>(o.aW, CK[B]);
+    sts_s32_off<kBufW<CB> + kCOff - 4 * T * B>(o.aWm, CK[B]);
     MS[B] = isp ? -MS[B] : MS[B];
     EX[B] = isp ? o.exp_new : EX[B];
-    if constexpr (B + 1 < NS) slot_asm<CB, B + 1>(o);
+    if constexpr (B + 1 < NS) slot_store<CB, B + 1>(o, v);
   }
 
   // apply_cb with explicit shared-window addressing: one IMAD per gather
   // base per step, every slot offset and buffer choice an immediate.
   template <int CB>
   __device__ __forceinline__ void apply_asm(int pos, int dEp, int t, int tenure) {
-    using SE = std::remove_pointer_t<decltype(sm->spins())>;
-    constexpr int e = sizeof(SE);
-    constexpr bool kS4 = e == 4;
+    constexpr int e = kE;
     sts_spin<e>(pend_a, pend_val);  // the previous flip's spin
     const uint32_t up = static_cast<uint32_t>(pos);
     const uint32_t a_sig = aS0 + e * up;
     const int sig16 = lds_spin<e, 0>(a_sig);
-    const int sig = sig16 >> 4;
+    const int sig = sig16 >> Sc::kSpinShift;
     StepOps o;
     o.nsig = -sig;
-    o.c32 = sig * 32;
+    o.c32 = sig16 + sig16;  // 4 kC sigma (kSpin = 2 kC)
     o.pos = pos;
     o.ln = tile_lane<T>();
     o.exp_new = t + tenure;
@@ -530,7 +587,9 @@ struct Walker {
     o.a6 = kS4 ? o.a3 : aQ + 4 * up;
     o.aW = kS4 ? aLp : aCp;
     o.aWm = kS4 ? aLm : aCm;
-    slot_asm<CB, 0>(o);
+    SlotIn v[NS];
+    slot_load<CB, 0>(o, v);   // every gather of the step ...
+    slot_store<CB, 0>(o, v);  // ... before any store (one C buffer)
     cb = CB ^ 1;
     pend_pos = pos;
     pend_a = a_sig;
@@ -649,7 +708,7 @@ __device__ __noinline__ Pick<R> tie_pick(SlotVals<NS> key, int dmin, int pos, R 
 // over the other keys; T < 32: one warp ballot of "same dE, other position",
 // i.e. 0 < key ^ kmin < 256); the tie set (ballots) is only built when it is
 // tied (or when FULL_TIES asks for it). Must be entered by the whole warp.
-template <int NS, int T, bool FULL_TIES, class R>
+template <int NS, int T, bool FULL_TIES, class R, bool KEYED = false>
 __device__ __forceinline__ void select_move(const int (&dE)[NS],
                                             const bool (&adm)[NS], int n,
                                             int tie_rule, R& rng, int& pos,
@@ -660,7 +719,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
   int kmin = INT_MAX;
 #pragma unroll
   for (int b = 0; b < NS; ++b) {
-    key.v[b] = adm[b] ? dE[b] * 256 + T * b + ln : INT_MAX;
+    key.v[b] = adm[b] ? (KEYED ? dE[b] : dE[b] * 256 + T * b + ln) : INT_MAX;
     kmin = min(kmin, key.v[b]);
   }
   kmin = tile_min_converged<T>(kmin);
@@ -676,11 +735,16 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
   if (kmin == INT_MAX) {
     SlotVals<NS> d;
 #pragma unroll
-    for (int b = 0; b < NS; ++b) d.v[b] = dE[b];
-    const Pick<R> f = fallback_pick<NS, T>(d, n, rng);
-    rng = f.rng;
-    pos = f.pos;
-    dEp = f.aux;
+    for (int b = 0; b < NS; ++b) d.v[b] = KEYED ? dE[b] >> 8 : dE[b];
+    if constexpr (LABS_RARE_INLINE) {
+      pos = uniform_below(rng, static_cast<uint32_t>(n));
+      dEp = at_position<NS, T>(d.v, pos);
+    } else {
+      const Pick<R> f = fallback_pick<NS, T>(d, n, rng);
+      rng = f.rng;
+      pos = f.pos;
+      dEp = f.aux;
+    }
     fallback = 1;
     ntie = 0;
 #pragma unroll
@@ -719,7 +783,7 @@ __device__ __forceinline__ void select_move(const int (&dE)[NS],
       tied = (k2 >> 8) == dmin;
     }
     if (tied) {
-      if constexpr (LABS_TIE_INLINE) {
+      if constexpr (LABS_TIE_INLINE || LABS_RARE_INLINE) {
         bool hit[NS];
         int cnt = 0;
 #pragma unroll
