@@ -171,6 +171,57 @@ def run_tts(ctx, n_values, targets, reps=5, replicas=0, base_seed=7, time_limit=
     return out
 
 
+def run_tts_islands(ctx, n_values, targets, reps, replicas, base_seed, time_limit,
+                    rng_kind=None, log=None, epoch_seconds=1.0):
+    """run_tts over every rank of the process group (one GPU per rank; the
+    island model of configs[4] without migration): sample s uses the global
+    seed block base + s * R * world, rank g owns global replicas g*R + r
+    (seeds base + id, proj/src/parallel.cpp:38). A target reached on any
+    rank stops every rank from the device (IPC peer stop flags); runtime =
+    max over ranks of creation -> stop."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_00987_b200 import capi
+    from paper_2504_00987_b200.islands import Islands
+    from paper_2504_00987_b200.sequence import encode_hex
+    rng_kind = capi.RNG_MT19937_64 if rng_kind is None else rng_kind
+    world, rank = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", ctx.device)
+    out, run = [], 0
+    for n in n_values:
+        R = replicas or capi.Solver.capacity(ctx, n, rng_kind)
+        for _ in range(reps):
+            seed = base_seed + run * R * world
+            run += 1
+            params = capi.memetic_params(target_energy=targets[n], max_seconds=time_limit + 5,
+                                         rng_kind=rng_kind)
+            dist.barrier()
+            t0 = time.perf_counter()
+            sv = capi.Solver(ctx, n, R, base_seed=seed, replica_offset=rank * R, params=params)
+            isl = Islands(sv, n, k_elites=1, device=dev)
+            rep = isl.run(targets[n], epoch_seconds=epoch_seconds, max_seconds=time_limit)
+            dt = time.perf_counter() - t0
+            t = torch.tensor([dt], dtype=torch.float64,
+                             device=dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e, r = rep.best_energy, rep.best_replica
+            seq = ""
+            if r // R == rank:
+                seq = encode_hex(sv.results()[r - rank * R]["best"], n)
+            seqs = [None] * world
+            dist.all_gather_object(seqs, seq)
+            isl.close()
+            sv.close()
+            rec = {"n": n, "targetE": targets[n], "runtime": float(t.item()),
+                   "reachedTarget": e <= targets[n], "seed": seed, "replicas": R * world,
+                   "gpus": world, "bestE": e, "bestSeq": next(x for x in seqs if x) if any(seqs)
+                   else "", "bestReplica": r}
+            out.append(rec)
+            if log and rank == 0:
+                log(rec)
+    return out
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--n", default="24-40", help="range a-b or comma list")
@@ -183,16 +234,42 @@ def main(argv=None):
     ap.add_argument("--fit", default=None, help="n_min-n_max window")
     ap.add_argument("--target-column", type=int, default=1,
                     help="energy column of --targets (targets_long.txt: 2 = previous best)")
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="island model over this many GPUs (one rank each; re-executes "
+                         "under torch.distributed.run when not already under it)")
     args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        import torch
+        if torch.cuda.device_count() < args.gpus:
+            sys.stderr.write(f"tts: --gpus {args.gpus} needs {args.gpus} CUDA devices; "
+                             f"{torch.cuda.device_count()} visible\n")
+            return 2
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", "-m", "paper_2504_00987_b200.tts"] + \
+            (argv if argv is not None else sys.argv[1:])
+        os.execv(sys.executable, cmd)
     if "-" in args.n:
         a, b = map(int, args.n.split("-"))
         ns = list(range(a, b + 1))
     else:
         ns = [int(x) for x in args.n.split(",")]
     from paper_2504_00987_b200 import capi
-    ctx = capi.Context(0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = capi.Context(local)
     targets = read_targets(args.targets, args.target_column)
-    fh = open(args.out, "a") if args.out else None
+    fh = open(args.out, "a") if args.out and rank == 0 else None
 
     def log(rec):
         line = json.dumps(rec, sort_keys=True)
@@ -201,10 +278,21 @@ def main(argv=None):
             fh.write(line + "\n")
             fh.flush()
 
-    samples = run_tts(ctx, ns, targets, args.reps, args.replicas, args.seed, args.time_limit,
-                      log=log)
+    if world > 1:
+        samples = run_tts_islands(ctx, ns, targets, args.reps, args.replicas, args.seed,
+                                  args.time_limit, log=log)
+        if rank != 0:
+            return 0
+    else:
+        samples = run_tts(ctx, ns, targets, args.reps, args.replicas, args.seed,
+                          args.time_limit, log=log)
     med = median_runtime_by_n(samples)
-    summary = {"medians": med,
+    quart = {}
+    for n in sorted({s["n"] for s in samples}):
+        t = [s["runtime"] for s in samples if s["n"] == n and s["reachedTarget"]]
+        quart[n] = {"q1": quantile(t, 0.25), "median": quantile(t, 0.5),
+                    "q3": quantile(t, 0.75), "uncensored": len(t)} if t else {"uncensored": 0}
+    summary = {"medians": med, "quartiles": quart,
                "censored": sum(not s["reachedTarget"] for s in samples)}
     if args.fit:
         lo, hi = map(int, args.fit.split("-"))

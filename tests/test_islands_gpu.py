@@ -51,6 +51,14 @@ def _worker(rank, world, port, mode, q):
                             for r in res],
                    "key": unpack_key(isl.global_best()[0]), "best": rep.best_energy,
                    "best_replica": rep.best_replica}
+        elif mode == "tts":
+            from paper_2504_00987_b200.tts import run_tts_islands
+            recs = run_tts_islands(ctx, [30], {30: 59}, reps=2, replicas=16, base_seed=900,
+                                   time_limit=60.0, epoch_seconds=0.2)
+            out = {"recs": recs}
+            q.put((rank, out))
+            dist.destroy_process_group()
+            return
         else:
             n, R, base, target = 37, 1, 2011, 86
             params = capi.memetic_params(target_energy=target)
@@ -128,3 +136,22 @@ def test_islands_world2_target_on_rank1_stops_rank0():
     assert r0["trace"][:-1] == ref["child_energies"][:r0["iterations"]]
     for r in (r0, r1):
         assert r["global_best"] == r1["best"] and r["global_replica"] == 1
+
+
+def test_tts_islands_world2():
+    """tts.run_tts_islands (the multi-rank TTS driver, `tts.py --gpus N`):
+    both ranks agree on every sample, seed blocks are disjoint across
+    samples (base + s * R * world), and every sample reaches the proven
+    optimum E=59 at n=30 with a sequence of that energy."""
+    from oracle.pyoracle import Oracle
+    from paper_2504_00987_b200.sequence import decode_hex
+    o = Oracle()
+    out = _run("tts")
+    r0, r1 = out[0]["recs"], out[1]["recs"]
+    assert len(r0) == len(r1) == 2
+    for a, b in zip(r0, r1):
+        assert {k: a[k] for k in a if k != "runtime"} == {k: b[k] for k in b if k != "runtime"}
+        assert a["runtime"] == b["runtime"]  # max over ranks
+        assert a["reachedTarget"] and a["bestE"] == 59 and a["gpus"] == 2
+        assert o.energy(30, decode_hex(a["bestSeq"], 30)) == 59
+    assert [r["seed"] for r in r0] == [900, 900 + 16 * 2]
