@@ -1,4 +1,11 @@
-"""Walker-count / occupancy sweep of the bare tabu kernel (BASELINE configs[3]).
+"""Walker-count / occupancy sweep (BASELINE configs[3]) of the product kernel
+K4 (`--kernel memetic`, default) or of the bare tabu kernel K3.
+
+K4 (labs_solver_run): W memetic replicas (reference MemeticParams, target
+unreachable), one warp each; above the resident capacity the grid stays
+capacity-sized and each warp serves its replicas in waves. A launch gives
+every replica `--epoch-ms` of device time; flip-evaluations/s = tabu
+iterations x n / launch time (CUDA events, best of --reps launches).
 
 K3 (`labs_tabu_walks_device`): W independent walkers, one warp each, each
 running `--walks` tabu_search walks back to back (walk k+1 starts from walk
@@ -22,7 +29,11 @@ def main(argv=None):
     ap.add_argument("--walks", type=int, default=20)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--rng", choices=["mt19937_64", "philox"], default="mt19937_64")
+    ap.add_argument("--kernel", choices=["memetic", "tabu"], default="memetic")
+    ap.add_argument("--epoch-ms", type=float, default=50.0)
     args = ap.parse_args(argv)
+    if args.kernel == "memetic":
+        return sweep_memetic(args)
 
     import numpy as np
     import torch
@@ -71,6 +82,42 @@ def main(argv=None):
         print(json.dumps(row), flush=True)
     cap = capi.Solver.capacity(ctx, n, kind)
     print(json.dumps({"resident_warps": cap, "sm_count": ctx.sm_count}), flush=True)
+    return 0
+
+
+def sweep_memetic(args):
+    import torch
+    from paper_2504_00987_b200 import capi
+
+    ctx = capi.Context(0)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", 0))
+    n = args.n
+    kind = capi.RNG_PHILOX if args.rng == "philox" else capi.RNG_MT19937_64
+    cap = capi.Solver.capacity(ctx, n, kind)
+    for W in [int(x) for x in args.walkers.split(",")]:
+        sv = capi.Solver(ctx, n, W, base_seed=42, params=capi.memetic_params(
+            target_energy=0, rng_kind=kind))
+        sv.run(epoch_seconds=args.epoch_ms / 1e3, race=False)  # init + warm-up
+        best = None
+        for _ in range(args.reps):
+            t_before, _ = sv.counters()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(ext):
+                e0.record(ext)
+            sv.run(epoch_seconds=args.epoch_ms / 1e3, race=False)
+            with torch.cuda.stream(ext):
+                e1.record(ext)
+            ctx.synchronize()
+            ms = e0.elapsed_time(e1)
+            t_after, _ = sv.counters()
+            rate = (t_after - t_before) * n / (ms / 1e3)
+            if best is None or rate > best[0]:
+                best = (rate, ms, t_after - t_before)
+        sv.close()
+        row = {"kernel": "k_memetic", "n": n, "replicas": W, "resident_capacity": cap,
+               "waves": -(-W // cap), "flip_evals_per_s": best[0], "launch_ms": best[1],
+               "tabu_iterations": best[2], "epoch_ms": args.epoch_ms, "rng": args.rng}
+        print(json.dumps(row), flush=True)
     return 0
 
 

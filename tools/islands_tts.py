@@ -3,7 +3,8 @@ exchange is replica-to-replica through k_export/k_import_elites; with more
 GPUs the same driver all_gathers elites over NCCL). Compare with
 `python -m paper_2504_00987_b200.tts` (no exchange) on the same instances.
 
-usage: python tools/islands_tts.py --n 98,99,104,107 --limit 180 --every 1 --epoch 1.0
+usage: python tools/islands_tts.py --n 98,99,104,107 --limit 180 --every 30 --epoch 1.0 \
+           --k 4 --replacement random      (--every 0: no exchange)
 """
 import argparse
 import json
@@ -27,6 +28,9 @@ def main():
     ap.add_argument("--epoch", type=float, default=1.0, help="epoch seconds")
     ap.add_argument("--k", type=int, default=16, help="elites per exchange")
     ap.add_argument("--seed", type=int, default=11)
+    ap.add_argument("--replacement", choices=["random", "worst"], default="random",
+                    help="population replacement: the reference's uniform victim "
+                         "(memetic.cpp:100-102) or elite-preserving worst member")
     ap.add_argument("--targets", default=os.path.join(ROOT, "paper_2504_00987_b200", "data",
                                                       "targets_long.txt"))
     ap.add_argument("--target-column", type=int, default=2)
@@ -39,7 +43,8 @@ def main():
     for n in [int(x) for x in a.n.split(",")]:
         R = capi.Solver.capacity(ctx, n, capi.RNG_MT19937_64)
         params = capi.memetic_params(target_energy=targets[n], max_seconds=a.limit + 5,
-                                     replacement=capi.REPLACE_WORST)
+                                     replacement=capi.REPLACE_WORST if a.replacement == "worst"
+                                     else capi.REPLACE_RANDOM)
         t0 = time.perf_counter()
         sv = capi.Solver(ctx, n, R, base_seed=a.seed, params=params)
         isl = Islands(sv, n, k_elites=a.k, device=torch.device("cuda", 0))
@@ -49,7 +54,8 @@ def main():
         rec = {"n": n, "targetE": targets[n], "bestE": rep.best_energy,
                "reachedTarget": rep.reached, "runtime": dt, "replicas": R,
                "exchange_every_epochs": a.every, "epoch_s": a.epoch, "k_elites": a.k,
-               "replacement": "worst", "seed": a.seed, "epochs": rep.epochs}
+               "replacement": a.replacement, "seed": a.seed, "epochs": rep.epochs,
+               "exchanges": rep.exchanges}
         sv.close()
         line = json.dumps(rec, sort_keys=True)
         print(line, flush=True)
