@@ -48,7 +48,7 @@ struct TileSlot {
   uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
   uint64_t out[MT ? kMtN : PhiloxRng::kBlock];  // tempered block / Philox block
   uint8_t tenure[MT ? kMtN : 4];  // MT: tenure table of the block (labs_rng.cuh)
-  int32_t tenure_par[2];          // MT: its window {min_t, range}
+  int32_t tenure_par[4];          // MT: {min_t, range, table window, pad}
   TileCtl ctl;
   WalkSmemL<L> walk;
 };
@@ -91,8 +91,10 @@ __device__ __forceinline__ void mt_load(uint64_t* s, uint64_t* out, const labs_r
                                         MtRngT<T>& rng) {
   for (int i = tile_lane<T>(); i < kMtN; i += T) s[i] = g.mt[i];
   if (tile_lane<T>() == 0) {  // tenure window {0, 1} until a walk sets one
-    reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(out) + kTenParOff)[0] = 0;
-    reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(out) + kTenParOff)[1] = 1;
+    int32_t* par = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(out) + kTenParOff);
+    par[0] = 0;
+    par[1] = 1;
+    par[2] = kTenWinMin;
   }
   tile_sync<T>();
   mt_temper_all<T>(s, out);

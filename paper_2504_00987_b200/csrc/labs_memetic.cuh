@@ -460,7 +460,7 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
           floor(__dadd_rn(__dmul_rn(A.tabu.min_factor, static_cast<double>(m)), 1e-9)));
       const int max_t = static_cast<int>(
           floor(__dadd_rn(__dmul_rn(A.tabu.max_factor, static_cast<double>(m)), 1e-9)));
-      rng.begin_walk(min_t, static_cast<uint32_t>(max_t - min_t + 1));
+      rng.begin_walk(min_t, static_cast<uint32_t>(max_t - min_t + 1), m);
       w.init(n, child, cb0);
       ctl.ran = 1;
       wbestE = w.E;

@@ -159,95 +159,100 @@ __device__ __forceinline__ void sts_u8(uint32_t saddr, uint32_t v) {
 // rebuilt from the current index when a walk starts (new window) and for
 // the whole block at every twist; windows with max_t > 254 are not cached.
 constexpr uint32_t kTenOff = 8u * kMtN;          // table offset from the block
-constexpr uint32_t kTenParOff = 8u * kMtN + kMtN;  // {min_t, range} (int32 x 2)
+constexpr uint32_t kTenParOff = 8u * kMtN + kMtN;  // {min_t, range, window} (int32)
 
-// Build table entries [lo, kMtN) from the tempered block; returns the first
-// index >= lo that is not cached (kMtN when all are).
+// Tenure entries are tabulated in windows (the tail of a block is usually
+// not reached by the walk that tabulated it): the window length, set per
+// walk from its step count, is the third parameter word.
+constexpr int kTenWinMin = 64;
+
+// Build table entries [lo, min(lo + window, kMtN)) from the tempered block;
+// returns the first index >= lo that is not served from the table (a
+// possibly-rejecting entry, or the window end).
 template <int T>
 __device__ __forceinline__ int mt_tenure_fill(uint32_t out, int lo) {
   const int min_t = lds_s32(out + kTenParOff);
   const uint32_t r32 = static_cast<uint32_t>(lds_s32(out + kTenParOff + 4));
   if (min_t + static_cast<int>(r32) - 1 > 254) return lo;
-  int first = kMtN;
+  const int win = lds_s32(out + kTenParOff + 8);
+  const int hi = lo + win < kMtN ? lo + win : kMtN;
+  int first = hi;
 #pragma unroll 1
-  for (int base = lo; base < kMtN; base += T) {
+  for (int base = lo; base < hi; base += T) {
     const int i = base + tile_lane<T>();
     bool rej = false;
-    if (i < kMtN) {
+    if (i < hi) {
       const uint64_t x = lds_u64(out + 8u * static_cast<uint32_t>(i));
       const uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
       const uint64_t p1 =
           static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
       rej = static_cast<uint32_t>(p1) == 0 && static_cast<uint32_t>(p0) < r32;
-      sts_u8(out + kTenOff + i, rej ? 0xFFu : static_cast<uint32_t>(min_t) +
-                                                  static_cast<uint32_t>(p1 >> 32));
+      sts_u8(out + kTenOff + i, static_cast<uint32_t>(min_t) + static_cast<uint32_t>(p1 >> 32));
     }
     const uint32_t b = tile_ballot<T>(rej);
-    if (b && first == kMtN) first = base + __ffs(b) - 1;
+    if (b) {
+      first = base + __ffs(b) - 1;
+      break;
+    }
   }
-  tile_sync<T>();
   return first;
 }
 
-// First index >= lo whose entry is not served from the table.
 template <int T>
-__device__ __noinline__ int mt_tenure_rescan(uint32_t out, int lo) {
-  const int min_t = lds_s32(out + kTenParOff);
-  const int r = lds_s32(out + kTenParOff + 4);
-  if (min_t + r - 1 > 254) return lo;
-#pragma unroll 1
-  for (int base = lo; base < kMtN; base += T) {
-    const int i = base + tile_lane<T>();
-    const uint32_t b = tile_ballot<T>(i < kMtN && lds_u8(out + kTenOff + i) == 0xFFu);
-    if (b) return base + __ffs(b) - 1;
-  }
-  return kMtN;
+__device__ __noinline__ int mt_tenure_window(uint32_t out, int lo) {
+  return mt_tenure_fill<T>(out, lo);
 }
 
 template <int T>
-__device__ __noinline__ int mt_tenure_table(uint32_t out, int lo, int min_t, uint32_t range) {
+__device__ __noinline__ int mt_tenure_table(uint32_t out, int lo, int min_t, uint32_t range,
+                                            int steps) {
   if (tile_lane<T>() == 0) {
     sts_s32(out + kTenParOff, min_t);
     sts_s32(out + kTenParOff + 4, static_cast<int32_t>(range));
+    // about one window per walk: its steps plus the expected tie draws
+    const int w = (steps + steps / 8 + 8 + 31) & ~31;
+    sts_s32(out + kTenParOff + 8, w < kTenWinMin ? kTenWinMin : (w > kMtN ? kMtN : w));
   }
   tile_sync<T>();
   return mt_tenure_fill<T>(out, lo);
 }
 
-// Twist, temper the new block, rebuild its tenure table; returns tc_hi.
+// Twist, temper the new block, tabulate its first tenure window; returns
+// tc_hi. Each lane's reads of a chunk are issued before its stores, and a
+// warp's shared-memory accesses execute in order, so no lane overwrites a
+// word another lane has yet to read (the tile is converged).
 template <int T>
 __device__ __noinline__ int mt_twist(uint32_t mt, uint32_t out) {
   const int lane = tile_lane<T>();
-  const unsigned tm = tile_mask<T>();
   // i in [0, 156): inputs mt[i], mt[i+1], mt[i+156], all old.
 #pragma unroll 1
   for (int base = 0; base < kMtN - kMtM; base += T) {
     const uint32_t i = base + lane;
-    uint64_t v = 0;
-    if (i < kMtN - kMtM)
-      v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)), lds_u64(mt + 8 * (i + kMtM)));
-    __syncwarp(tm);
-    if (i < kMtN - kMtM) sts_u64(mt + 8 * i, v);
-    __syncwarp(tm);
+    if (i < kMtN - kMtM) {
+      const uint64_t v =
+          mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)), lds_u64(mt + 8 * (i + kMtM)));
+      sts_u64(mt + 8 * i, v);
+      sts_u64(out + 8 * i, mt_temper(v));
+    }
   }
   // i in [156, 311): inputs mt[i], mt[i+1] old, mt[i-156] new.
 #pragma unroll 1
   for (int base = kMtN - kMtM; base < kMtN - 1; base += T) {
     const uint32_t i = base + lane;
-    uint64_t v = 0;
-    if (i < kMtN - 1)
-      v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)),
-                 lds_u64(mt + 8 * (i - (kMtN - kMtM))));
-    __syncwarp(tm);
-    if (i < kMtN - 1) sts_u64(mt + 8 * i, v);
-    __syncwarp(tm);
+    if (i < kMtN - 1) {
+      const uint64_t v = mt_mix(lds_u64(mt + 8 * i), lds_u64(mt + 8 * (i + 1)),
+                                lds_u64(mt + 8 * (i - (kMtN - kMtM))));
+      sts_u64(mt + 8 * i, v);
+      sts_u64(out + 8 * i, mt_temper(v));
+    }
   }
-  if (lane == 0)
-    sts_u64(mt + 8 * (kMtN - 1),
-            mt_mix(lds_u64(mt + 8 * (kMtN - 1)), lds_u64(mt), lds_u64(mt + 8 * (kMtM - 1))));
-  __syncwarp(tm);
-  for (int i = lane; i < kMtN; i += T) sts_u64(out + 8 * i, mt_temper(lds_u64(mt + 8 * i)));
-  __syncwarp(tm);
+  if (lane == 0) {
+    const uint64_t v =
+        mt_mix(lds_u64(mt + 8 * (kMtN - 1)), lds_u64(mt), lds_u64(mt + 8 * (kMtM - 1)));
+    sts_u64(mt + 8 * (kMtN - 1), v);
+    sts_u64(out + 8 * (kMtN - 1), mt_temper(v));
+  }
+  tile_sync<T>();
   return mt_tenure_fill<T>(out, 0);
 }
 
@@ -298,8 +303,8 @@ struct MtRngT {
   }
   // A walk's tenure window [min_t, min_t + range): tabulate the rest of the
   // block for it.
-  __device__ __forceinline__ void begin_walk(int min_t, uint32_t range) {
-    tc_hi = mt_tenure_table<T>(out_s, idx < kMtN ? idx : kMtN, min_t, range);
+  __device__ __forceinline__ void begin_walk(int min_t, uint32_t range, int steps) {
+    tc_hi = mt_tenure_table<T>(out_s, idx < kMtN ? idx : kMtN, min_t, range, steps);
   }
   // uniform_int(min_t, min_t + range - 1): one table byte, or the full draw.
   __device__ __forceinline__ int tenure();
@@ -386,7 +391,7 @@ struct PhiloxRngT {
   }
   int tmin;        // the walk's tenure window (begin_walk)
   uint32_t trange;
-  __device__ __forceinline__ void begin_walk(int min_t, uint32_t range) {
+  __device__ __forceinline__ void begin_walk(int min_t, uint32_t range, int /*steps*/) {
     tmin = min_t;
     trange = range;
   }
@@ -464,6 +469,8 @@ struct TenurePick {
 };
 template <int T>
 __device__ __noinline__ TenurePick<T> mt_tenure_slow(MtRngT<T> r);
+template <int T>
+__device__ __forceinline__ TenurePick<T> mt_tenure_slow_body(MtRngT<T> r);
 
 template <int T>
 __device__ __forceinline__ int MtRngT<T>::tenure() {
@@ -473,11 +480,9 @@ __device__ __forceinline__ int MtRngT<T>::tenure() {
     return v;
   }
 #if LABS_RARE_INLINE
-  const int min_t = lds_s32(out_s + kTenParOff);
-  const uint32_t range = static_cast<uint32_t>(lds_s32(out_s + kTenParOff + 4));
-  const int v = min_t + uniform_below(*this, range);
-  tc_hi = idx < kMtN ? mt_tenure_rescan<T>(out_s, idx) : kMtN;
-  return v;
+  const TenurePick<T> p = mt_tenure_slow_body<T>(*this);
+  *this = p.rng;
+  return p.v;
 #else
   const TenurePick<T> p = mt_tenure_slow<T>(*this);
   *this = p.rng;
@@ -506,13 +511,31 @@ __device__ __forceinline__ int PhiloxRngT<T>::tenure() {
   return tmin + uniform_below(*this, trange);
 }
 
+// Outside the tabulated window: at the block end twist (which tabulates the
+// new block's first window), at a window end tabulate the next window; a
+// possibly-rejecting entry takes the full uniform_int.
 template <int T>
-__device__ __noinline__ TenurePick<T> mt_tenure_slow(MtRngT<T> r) {
+__device__ __forceinline__ TenurePick<T> mt_tenure_slow_body(MtRngT<T> r) {
+  if (r.idx >= kMtN) {
+    r.tc_hi = mt_twist<T>(r.mt_s, r.out_s);
+    r.idx = 0;
+  }
+  if (r.idx >= r.tc_hi) r.tc_hi = mt_tenure_window<T>(r.out_s, r.idx);
+  if (r.idx < r.tc_hi) {
+    const int v = static_cast<int>(lds_u8(r.out_s + kTenOff + static_cast<uint32_t>(r.idx)));
+    ++r.idx;
+    return {v, r};
+  }
   const int min_t = lds_s32(r.out_s + kTenParOff);
   const uint32_t range = static_cast<uint32_t>(lds_s32(r.out_s + kTenParOff + 4));
   const int v = min_t + uniform_below(r, range);
-  r.tc_hi = r.idx < kMtN ? mt_tenure_rescan<T>(r.out_s, r.idx) : kMtN;
+  r.tc_hi = r.idx < kMtN ? mt_tenure_window<T>(r.out_s, r.idx) : r.idx;
   return {v, r};
+}
+
+template <int T>
+__device__ __noinline__ TenurePick<T> mt_tenure_slow(MtRngT<T> r) {
+  return mt_tenure_slow_body<T>(r);
 }
 
 template <class R>

@@ -371,12 +371,14 @@ def test_solve_cli_wire_format(tmp_path):
 
 
 @pytest.mark.parametrize("n,lo,hi,iters", [(60, 0.10, 0.90, 6), (200, 0.0, 0.95, 2),
-                                           (33, 0.0, 0.0, 8)])
+                                           (33, 0.0, 0.0, 8), (256, 0.5, 0.99, 3),
+                                           (119, 0.10, 0.12, 40), (64, 0.10, 0.12, 60)])
 def test_memetic_wide_tenure_windows(ctx, oracle, n, lo, hi, iters):
     """Tenure windows far from the default 0.10/0.12 (wide ones exercise the
     range-specialized Lemire reduction with large ranges; a one-value window
-    still consumes one draw per step). Whole memetic runs must replay the
-    oracle draw for draw."""
+    still consumes one draw per step; max_t > 254 is served without the
+    tenure table), and long default runs that cross many table windows and
+    MT twists. Whole memetic runs must replay the oracle draw for draw."""
     kw = dict(min_tabu_factor=lo, max_tabu_factor=hi)
     want = oracle.memetic(n, 4242, child_cap=iters, max_iterations=iters, **kw)
     d = ctx.memetic(n, 4242, capi.memetic_params(max_iterations=iters, **kw), trace_cap=iters + 1)
