@@ -255,15 +255,26 @@ def main():
     import torch.distributed as dist
     from paper_2504_00987_b200 import capi
 
+    # LABS_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 with gloo
+    # collectives, to exercise the multi-rank code path on a one-GPU box; the
+    # ranks' kernels never wait on one another, and the number is not a
+    # scaling measurement.
+    one_dev = os.environ.get("LABS_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     if torch.cuda.device_count() <= local:
         sys.stderr.write(f"bench.py: rank {rank} needs cuda:{local}; "
                          f"{torch.cuda.device_count()} device(s) visible\n")
         sys.exit(2)
     torch.cuda.set_device(local)
+    cdev = "cpu" if one_dev else f"cuda:{local}"  # collective tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
-        sys.stderr.write(f"bench.py: rank {rank}/{world} on cuda:{local}, NCCL communicator "
+        sys.stderr.write(f"bench.py: rank {rank}/{world} on cuda:{local}, communicator "
                          f"up (backend {dist.get_backend()})\n")
     ctx = capi.Context(local)
     ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
@@ -313,7 +324,7 @@ def main():
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     evals_local = float(t_after - t_before) * n
     if world > 1:
-        tt = torch.tensor([evals_local, dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+        tt = torch.tensor([evals_local, dev_ms], dtype=torch.float64, device=cdev)
         ev = tt[:1].clone()
         dist.all_reduce(ev, op=dist.ReduceOp.SUM)
         mx = tt[1:].clone()
@@ -360,7 +371,7 @@ def main():
     e2e_evals = sum(p["tabu_iterations"] for p in per) * n
     e2e_value = e2e_evals / e2e_t
     if world > 1:
-        t = torch.tensor([e2e_evals, e2e_t], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([e2e_evals, e2e_t], dtype=torch.float64, device=cdev)
         a = t[:1].clone()
         dist.all_reduce(a)
         b = t[1:].clone()

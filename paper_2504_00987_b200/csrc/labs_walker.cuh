@@ -173,13 +173,15 @@ struct WalkSmemL {
     else return S;
   }
   // Packed bit windows for the O(n^2/32) popcount build: B32 holds s
-  // (position x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}).
+  // (position x at word (x + L) >> 5), R32 the reversed s (R_x = s_{n-1-x}),
+  // V32 the validity mask (1 on [0, n)), all zero-padded, so a shifted
+  // window of V32 masks exactly the valid pairs of a shifted window of s.
   // With two C buffers they alias the buffer that is idle until the walk's
   // first step; with one they (and the h build's int8 C) use W.
   static constexpr int kBitWords = 3 * NC + 2;
-  static_assert(2 * kBitWords <= 2 * L, "bit windows must fit one C buffer");
+  static_assert(3 * kBitWords <= 2 * L, "bit windows must fit one C buffer");
   static constexpr int kScratchWords =
-      LABS_SINGLE_C ? (2 * kBitWords > (L + 4 + 3) / 4 ? 2 * kBitWords : (L + 4 + 3) / 4) : 1;
+      LABS_SINGLE_C ? (3 * kBitWords > (L + 4 + 3) / 4 ? 3 * kBitWords : (L + 4 + 3) / 4) : 1;
   uint32_t W[kScratchWords];
   __device__ __forceinline__ uint32_t* scratch(int buf) {
     if constexpr (LABS_SINGLE_C) return W;
@@ -187,14 +189,19 @@ struct WalkSmemL {
   }
   __device__ __forceinline__ uint32_t* B32(int buf) { return scratch(buf); }
   __device__ __forceinline__ uint32_t* R32(int buf) { return B32(buf) + kBitWords; }
-  // Zero both windows of buffer `buf` and store the payload chunks of s.
+  __device__ __forceinline__ uint32_t* V32(int buf) { return B32(buf) + 2 * kBitWords; }
+  // Zero the windows of buffer `buf`, store the payload chunks of s and the
+  // validity mask.
   template <int T>
   __device__ __forceinline__ void put_bits(int n, const uint32_t* in, int buf) {
     uint32_t* b = B32(buf);
-    for (int i = tile_lane<T>(); i < 2 * kBitWords; i += T) b[i] = 0u;
+    for (int i = tile_lane<T>(); i < 3 * kBitWords; i += T) b[i] = 0u;
     tile_sync<T>();
     if (tile_lane<T>() == 0)
-      for (int c = 0; c < NC; ++c) b[NC + c] = in[c] & lowmask(n - 32 * c);
+      for (int c = 0; c < NC; ++c) {
+        b[NC + c] = in[c] & lowmask(n - 32 * c);
+        b[2 * kBitWords + NC + c] = lowmask(n - 32 * c);
+      }
     tile_sync<T>();
   }
 };
@@ -289,6 +296,7 @@ struct Walker {
     s.template put_bits<T>(n, in, scratch);
     uint32_t* B32 = s.B32(scratch);
     uint32_t* R32 = s.R32(scratch);
+    const uint32_t* V32 = s.V32(scratch);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       uint32_t word = 0;
@@ -314,7 +322,7 @@ struct Walker {
         for (int cc = 0; cc < NC; ++cc) {
           const uint32_t a = B32[NC + cc];
           const uint32_t x = window32<NC>(B32, 32 * cc + k);
-          acc += __popc((a ^ x) & lowmask(len - 32 * cc));
+          acc += __popc((a ^ x) & window32<NC>(V32, 32 * cc + k));  // pairs i + k < n
         }
         c = len - 2 * acc;
       }
@@ -353,11 +361,11 @@ struct Walker {
         int acc = 0;
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc) {
-          const uint32_t vm = lowmask(hi - 32 * cc + 1) & ~lowmask(lo - 32 * cc);
-          if (vm) {
-            const uint32_t x = window32<NC>(R32, n - 1 - m + 32 * cc);
-            acc += __popc((B32[NC + cc] ^ x) & vm);
-          }
+          // s_i against s_{m-i} = R_{n-1-m+i}; the pair is valid where both
+          // validity windows are set (i in [lo, hi])
+          const int o = n - 1 - m + 32 * cc;
+          const uint32_t x = window32<NC>(R32, o);
+          acc += __popc((B32[NC + cc] ^ x) & V32[NC + cc] & window32<NC>(V32, o));
         }
         qv = (hi - lo + 1) - 2 * acc;
       }
