@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--n", "--length", dest="n", type=int, default=64)
     ap.add_argument("--epoch-ms", type=float, default=100.0)
     ap.add_argument("--rng", choices=["mt19937_64", "philox"], default="mt19937_64")
     ap.add_argument("--replicas", type=int, default=0, help="0 = resident capacity")
@@ -143,9 +143,13 @@ def maybe_spawn(args):
             sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices; "
                              f"{have} visible\n")
             sys.exit(2)
+    # torchrun's own parser would take "--n" for an abbreviation of one of its
+    # options: pass the sequence length as --length
+    fwd = ["--length" if a == "--n" else ("--length=" + a[4:] if a.startswith("--n=") else a)
+           for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + fwd
     sys.stderr.write("bench.py: launching " + " ".join(cmd[1:6]) + "\n")
     sys.stderr.flush()
     os.execv(sys.executable, cmd)
@@ -348,8 +352,10 @@ def main():
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            per_ms = pj.get(f"k_memetic_n{n}_dram_bytes_per_ms")
-            traffic = per_ms * (time_ms / args.steps) if per_ms else None
+            # DRAM bytes of one k_memetic launch: replica state in and out
+            # (MT states, populations), nearly independent of the launch
+            # length (16.4 MB at 20 ms, 16.8 MB at 50 ms, N=64)
+            traffic = pj.get(f"k_memetic_n{n}_dram_bytes")
             issue = pj.get(f"k_memetic_n{n}_issue_slots_busy")
             prof_src = pj.get("source")
         except Exception:
@@ -397,8 +403,9 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "int32", "achieved": lag_gmacs, "peak": imad_peak,
                      "unit": "Gop/s", "frac": lag_gmacs / imad_peak, "traffic": traffic,
-                     "traffic_source": (f"extrapolated_from_ncu ({prof_src}): DRAM bytes per "
-                                        "ms of k_memetic x this run's launch length")
+                     "traffic_source": (f"from_ncu ({prof_src}): dram__bytes_read + write of one "
+                                        "k_memetic launch (per-launch replica state traffic; "
+                                        "not measured inside this run)")
                      if traffic is not None else None,
                      "work_per_flip_eval": f"{n - 1} lag-term MACs (N-1, SURVEY.md §8d)",
                      "peak_source": "IMAD-only probe labs_bench_imad_peak, measured on "

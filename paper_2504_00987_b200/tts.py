@@ -224,7 +224,7 @@ def run_tts_islands(ctx, n_values, targets, reps, replicas, base_seed, time_limi
 
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
-    ap.add_argument("--n", default="24-40", help="range a-b or comma list")
+    ap.add_argument("--n", "--lengths", dest="n", default="24-40", help="range a-b or comma list")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--targets", default=os.path.join(HERE, "data", "optima.txt"))
     ap.add_argument("--replicas", type=int, default=0)
@@ -251,7 +251,7 @@ def main(argv=None):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
                f"--master-port={port}", "-m", "paper_2504_00987_b200.tts"] + \
-            (argv if argv is not None else sys.argv[1:])
+            ["--lengths" if a == "--n" else a for a in (argv if argv is not None else sys.argv[1:])]
         os.execv(sys.executable, cmd)
     if "-" in args.n:
         a, b = map(int, args.n.split("-"))

@@ -19,7 +19,7 @@ def test_bench_two_ranks_one_device():
                         "--nproc-per-node=2", "--master-addr", "127.0.0.1",
                         "--master-port", "29633", os.path.join(ROOT, "bench.py"), "--gpus", "2",
                         "--quick", "--steps", "2", "--warmup", "1", "--epoch-ms", "20",
-                        "--n", "40", "--replicas", "256"],
+                        "--length", "40", "--replicas", "256"],
                        capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-4000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
