@@ -51,6 +51,20 @@ def _worker(rank, world, port, mode, q):
                             for r in res],
                    "key": unpack_key(isl.global_best()[0]), "best": rep.best_energy,
                    "best_replica": rep.best_replica}
+        elif mode == "exchange":
+            import numpy as np
+            n, R = 40, 6
+            params = capi.memetic_params(target_energy=0, max_iterations=10)
+            sv = capi.Solver(ctx, n, R, base_seed=700, replica_offset=rank * R, params=params)
+            sv.run(epoch_iterations=2, race=False)  # still running: imports apply
+            isl = Islands(sv, n, k_elites=2, device=torch.device("cuda", 0))
+            _, e_before = sv.population()
+            isl.exchange(rotation=1)
+            torch.cuda.synchronize()
+            sv.sync()
+            _, e_after = sv.population()
+            out = {"exported": isl.el_e.cpu().tolist(), "gathered": isl.all_e.cpu().tolist(),
+                   "before": e_before.tolist(), "after": e_after.tolist()}
         elif mode == "tts":
             from paper_2504_00987_b200.tts import run_tts_islands
             recs = run_tts_islands(ctx, [30], {30: 59}, reps=2, replicas=16, base_seed=900,
@@ -155,3 +169,24 @@ def test_tts_islands_world2():
         assert a["reachedTarget"] and a["bestE"] == 59 and a["gpus"] == 2
         assert o.energy(30, decode_hex(a["bestSeq"], 30)) == 59
     assert [r["seed"] for r in r0] == [900, 900 + 16 * 2]
+
+
+def test_islands_world2_exchange_imports_exported_elites():
+    """ADVICE r1 (stream race): after one exchange every rank holds exactly
+    the elites the two ranks exported (rank order), and each replica's worst
+    population member was replaced by its offered elite iff strictly better
+    (k_import_elites) — never by an unfilled buffer."""
+    out = _run("exchange")
+    gathered = out[0]["exported"] + out[1]["exported"]
+    for rank in (0, 1):
+        assert out[rank]["gathered"] == gathered
+        assert sorted(out[rank]["exported"]) == out[rank]["exported"]
+        R, count = len(out[rank]["before"]), len(gathered)
+        for r in range(R):
+            before, after = out[rank]["before"][r], out[rank]["after"][r]
+            elite = gathered[(r + 1) % count]
+            worst = max(range(len(before)), key=lambda i: (before[i], -i))
+            want = list(before)
+            if elite < before[worst]:
+                want[worst] = elite
+            assert after == want, (rank, r)
