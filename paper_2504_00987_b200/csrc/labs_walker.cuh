@@ -24,22 +24,26 @@
 // tests/test_oracle_cpu.py::test_incremental_identities; device parity:
 // tests/test_parity_gpu.py).
 //
-// Register layout per slot: D = dE_j itself, MS = -s_j, EX = expiry,
-// CK = C_j. With H = 4 h_j and HQ = 4 (n - 2 + Q_{2j}), dE_j = HQ + MS H, so
-// a committed flip p changes D by
-//   j != p:  dHQ + MS dH = c16 s_{2j-p} + MS (16 s_{2p-j} + c8 (2 C_{|j-p|}
-//            + Q_{p+j})) - 32          (MS^2 = 1; c_k = -k sigma)
+// Register layout per slot: D = dE_j itself (for L <= 64 the argmin key
+// 256 dE_j + j), MS = -s_j, EX = expiry, CK = C_j. With H = 4 h_j and
+// HQ = 4 (n - 2 + Q_{2j}), dE_j = HQ + MS H, so a committed flip p changes D
+// by
+//   j != p:  dHQ + MS dH = -16 sigma s_{2j-p} + MS (16 s_{2p-j} - 8 sigma
+//            (2 C_{|j-p|} + Q_{p+j})) - 32          (MS^2 = 1)
 //   j == p:  D -> -D                   (flipping p back undoes the move)
-// so neither h nor Q_{2j} is kept per slot.
+// so neither h nor Q_{2j} is kept per slot. The operands are stored
+// pre-scaled (WalkScales: spins x16, C and Q x8, all x256 more when keyed)
+// so the update multiplies by sigma alone.
 // Shared layout per walker: C mirrored as C2[L + d] = C_{|d|} so the gather
-// C_{|j-p|} is one LDS at a per-step base + 128 b, double-buffered (a step
-// reads one buffer and writes the other); Q[m]; spins as a zero-padded array
+// C_{|j-p|} is one LDS at a per-step base + 128 b (one buffer: a step issues
+// all its gathers before any store); Q[m]; spins as a zero-padded array
 // S[SO + x] (int8; int32 for walkers of L <= 64) so s_x for any x in
-// (-L-4, 2L+4) is one LDS with the range check folded into the padding. The flipped spin is stored by every lane at the
-// start of the next step (each lane then reads its own store), so a tabu
-// step needs a single warp barrier. Invalid positions (j >= n) keep EX = INT_MAX
-// (never admissible) and s_j = 0, which makes every update they perform a
-// no-op on the entries valid lanes read.
+// (-L-4, 2L+4) is one LDS with the range check folded into the padding. The
+// flipped spin is stored at the start of the next step. The warp is
+// converged through the step and its shared-memory accesses execute in
+// order, so the step needs no barrier. Invalid positions (j >= n) keep
+// EX = INT_MAX (never admissible) and s_j = 0, which makes every update they
+// perform a no-op on the entries valid lanes read.
 #pragma once
 #include <climits>
 #include <cstddef>
