@@ -147,6 +147,18 @@ int labs_build_state(labs_ctx* ctx, int n, int count, const uint64_t* words,
                      int32_t* corr_out, int64_t* energy_out,
                      int64_t* neighbor_out);
 
+/* Persistent single-sequence evaluator behind the C++ CorrelationState
+ * (correlation_state.hpp:17-36; .cpp:9-98): device and pinned host buffers
+ * are allocated once, so each evaluation (construction or apply_flip) is one
+ * H2D, one launch, one D2H and a synchronization. Outputs as
+ * labs_build_state with count = 1 (corr_out / neighbor_out may be NULL).
+ * For long flip sequences use labs_flip_trace (one launch for all flips). */
+typedef struct labs_eval labs_eval;
+int labs_eval_create(labs_ctx* ctx, int n, labs_eval** out);
+int labs_eval_destroy(labs_eval* e);
+int labs_eval_run(labs_eval* e, const uint64_t* words, int32_t* corr_out,
+                  int64_t* energy_out, int64_t* neighbor_out);
+
 /* Replaces a sequence of CorrelationState::apply_flip calls
  * (correlation_state.cpp:73-98): for each sequence, commit `flips` positions
  * (count x flips, row-major) in order; after flip f report the energy

@@ -4,7 +4,10 @@
 // The reference keeps a packed product table and answers neighbor_energy(j)
 // with an O(n) walk over it. Here the state is evaluated on the B200: a build
 // (or commit) runs the device engine once and caches C_k, E and all n
-// neighbor energies, so neighbor_energy(j) is a lookup. `touches` keeps the
+// neighbor energies, so neighbor_energy(j) is a lookup. Each object owns a
+// persistent device evaluator (labs_eval: no allocation per commit; one
+// H2D + launch + D2H). A commit is still a device round trip: callers that
+// flip long known sequences should batch them with labs_flip_trace. `touches` keeps the
 // reference's accounting (n-1 product entries per query or flip) so callers
 // that budget work with it see the same numbers.
 #pragma once
@@ -12,10 +15,13 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <vector>
 
 #include "labsolve/rng.hpp"
 #include "labsolve/sequence.hpp"
+
+struct labs_eval;  // the device evaluator (include/labs_b200.h)
 
 namespace labsolve {
 
@@ -40,6 +46,9 @@ class CorrelationState {
 
   int n_ = 0;
   Sequence pivot_;
+  // device scratch shared by copies (every evaluation re-uploads the pivot;
+  // the results live in the members below)
+  std::shared_ptr<::labs_eval> eval_;
   std::vector<std::int32_t> corr_;
   std::vector<long long> neighbors_;
   long long energy_ = 0;

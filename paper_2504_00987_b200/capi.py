@@ -50,6 +50,7 @@ EXPORTS = [
     "labs_solver_population", "labs_solver_state_size", "labs_solver_save", "labs_solver_load",
     "labs_solver_stop_flag", "labs_solver_set_peer_stops", "labs_ipc_export", "labs_ipc_open",
     "labs_ipc_close", "labs_run_replicas_multi", "labs_bench_imad_peak",
+    "labs_eval_create", "labs_eval_destroy", "labs_eval_run",
 ]
 CROSSOVER_UNIFORM = 0
 CROSSOVER_ONE_POINT = 1
@@ -186,6 +187,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                             C.c_int]
     L.labs_bench_int_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     L.labs_bench_imad_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.labs_eval_create.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.labs_eval_destroy.argtypes = [C.c_void_p]
+    L.labs_eval_run.argtypes = [C.c_void_p, u64p, i32p, i64p, i64p]
     L.labs_exhaustive_optimum.argtypes = [C.c_void_p, C.c_int, i64p, u64p, C.c_int64, i64p]
     L.labs_local_optima.argtypes = [C.c_void_p, C.c_int, i64p]
     L.labs_solver_population.argtypes = [C.c_void_p, u64p, i32p]
@@ -475,6 +479,36 @@ def run_replicas_multi(ctxs, n: int, replicas: int, base_seed: int,
                                  int(tr[r * trace_cap + i].child_energy))
                                 for i in range(min(int(tl[r]), trace_cap))]
     return res, reps
+
+
+class Evaluator:
+    """labs_eval: persistent single-sequence evaluator (C_k, E, neighbors)."""
+
+    def __init__(self, ctx: Context, n: int):
+        self.L, self.n = ctx.L, n
+        h = C.c_void_p()
+        _check(self.L.labs_eval_create(ctx.h, n, C.byref(h)))
+        self.h = h
+
+    def __call__(self, words):
+        w = _words(words, self.n)
+        corr = np.zeros(max(self.n - 1, 1), dtype=np.int32)
+        e = C.c_int64(0)
+        nb = np.zeros(self.n, dtype=np.int64)
+        _check(self.L.labs_eval_run(self.h, _ptr(w, u64p), _ptr(corr, i32p), C.byref(e),
+                                    _ptr(nb, i64p)))
+        return corr[:self.n - 1], int(e.value), nb
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.labs_eval_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Solver:

@@ -9,6 +9,9 @@ namespace labsolve {
 
 CorrelationState::CorrelationState(const Sequence& s) : n_(s.size()), pivot_(s) {
   if (n_ < 2) throw std::invalid_argument("correlation state needs length >= 2");
+  labs_eval* e = nullptr;
+  detail::check(labs_eval_create(detail::device(), n_, &e));
+  eval_ = std::shared_ptr<labs_eval>(e, labs_eval_destroy);
   evaluate();
 }
 
@@ -16,12 +19,10 @@ CorrelationState::CorrelationState(const Sequence& s) : n_(s.size()), pivot_(s) 
 void CorrelationState::evaluate() {
   corr_.assign(n_ - 1, 0);
   neighbors_.assign(n_, 0);
-  std::vector<int64_t> nb(n_);
   int64_t e = 0;
-  detail::check(labs_build_state(detail::device(), n_, 1, pivot_.data(), corr_.data(), &e,
-                                 nb.data()));
+  detail::check(labs_eval_run(eval_.get(), pivot_.data(), corr_.data(), &e,
+                              reinterpret_cast<int64_t*>(neighbors_.data())));
   energy_ = e;
-  for (int j = 0; j < n_; ++j) neighbors_[j] = nb[j];
 }
 
 long long CorrelationState::correlation(int k) const {

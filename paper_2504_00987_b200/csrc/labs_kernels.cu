@@ -244,6 +244,72 @@ int labs_build_state(labs_ctx* ctx, int n, int count, const uint64_t* words,
   return LABS_OK;
 }
 
+// Persistent evaluator for one sequence (labs_eval_*): the device buffer and
+// a pinned host mirror, laid out [words | E | neighbors | C], so one call is
+// one H2D, one launch, one D2H and a sync — no allocation per call.
+struct labs_eval {
+  labs_ctx* ctx = nullptr;
+  int n = 0, nw = 0;
+  void* d = nullptr;
+  unsigned char* h = nullptr;
+  size_t bytes = 0, off_e = 0, off_nb = 0, off_c = 0;
+  ~labs_eval() {
+    if (d) {
+      cudaSetDevice(ctx->device);
+      cudaFree(d);
+    }
+    if (h) cudaFreeHost(h);
+  }
+};
+
+int labs_eval_create(labs_ctx* ctx, int n, labs_eval** out) {
+  if (int rc = check_n(n)) return rc;
+  if (!ctx || !out) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  auto* e = new labs_eval;
+  std::unique_ptr<labs_eval> guard(e);
+  e->ctx = ctx;
+  e->n = n;
+  e->nw = nw_of(n);
+  e->off_e = sizeof(uint64_t) * e->nw;
+  e->off_nb = e->off_e + sizeof(int64_t);
+  e->off_c = e->off_nb + sizeof(int64_t) * n;
+  e->bytes = e->off_c + sizeof(int32_t) * (n - 1);
+  LABS_CUDA(cudaMalloc(&e->d, e->bytes));
+  LABS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h), e->bytes));
+  *out = guard.release();
+  return LABS_OK;
+}
+
+int labs_eval_destroy(labs_eval* e) {
+  delete e;
+  return LABS_OK;
+}
+
+int labs_eval_run(labs_eval* e, const uint64_t* words, int32_t* corr_out, int64_t* energy_out,
+                  int64_t* neighbor_out) {
+  if (!e || !words || !energy_out) return fail(LABS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (int rc = check_seq_padding(e->n, 1, words)) return rc;
+  labs_ctx* ctx = e->ctx;
+  LABS_CUDA(cudaSetDevice(ctx->device));
+  std::memcpy(e->h, words, sizeof(uint64_t) * e->nw);
+  unsigned char* d = static_cast<unsigned char*>(e->d);
+  LABS_H2D(d, e->h, sizeof(uint64_t) * e->nw);
+  const int n = e->n;
+  int rc = dispatch(n, [&](auto ns) -> int {
+    return NsOps<decltype(ns)::value>::build(
+        ctx, n, 1, reinterpret_cast<const uint64_t*>(d), reinterpret_cast<int32_t*>(d + e->off_c),
+        reinterpret_cast<int64_t*>(d + e->off_e), reinterpret_cast<int64_t*>(d + e->off_nb));
+  });
+  if (rc) return rc;
+  LABS_D2H(e->h + e->off_e, d + e->off_e, e->bytes - e->off_e);
+  LABS_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(energy_out, e->h + e->off_e, sizeof(int64_t));
+  if (neighbor_out) std::memcpy(neighbor_out, e->h + e->off_nb, sizeof(int64_t) * n);
+  if (corr_out) std::memcpy(corr_out, e->h + e->off_c, sizeof(int32_t) * (n - 1));
+  return LABS_OK;
+}
+
 int labs_flip_trace(labs_ctx* ctx, int n, int count, const uint64_t* words, int flips,
                     const int32_t* positions, int64_t* energy_out, int64_t* neighbor_out) {
   if (int rc = check_n(n)) return rc;

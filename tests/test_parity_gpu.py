@@ -386,3 +386,27 @@ def test_memetic_wide_tenure_windows(ctx, oracle, n, lo, hi, iters):
     assert d["best"].tolist() == want["best"]
     assert d["iterations"] == want["iterations"]
     assert [t[2] for t in d["trace"]] == want["child_energies"]
+
+
+@pytest.mark.parametrize("n", [2, 13, 64, 92, 119, 256])
+def test_evaluator_matches_build_state(ctx, oracle, n):
+    """labs_eval (the persistent evaluator behind CorrelationState) equals the
+    batch build and the oracle for consecutive flips of one sequence; a
+    commit costs one round trip (reported, not asserted)."""
+    import time
+    from paper_2504_00987_b200.sequence import random_words
+    rs = np.random.default_rng(n)
+    w = random_words(n, 1, rs)[0].copy()
+    ev = capi.Evaluator(ctx, n)
+    t0 = time.perf_counter()
+    flips = 40
+    for f in range(flips):
+        corr, e, nb = ev(w)
+        c2, e2, nb2 = ctx.build_state(n, w)
+        assert e == int(e2[0]) == oracle.energy(n, w)
+        assert corr.tolist() == c2[0].tolist() and nb.tolist() == nb2[0].tolist()
+        j = int(rs.integers(0, n))
+        w[j // 64] ^= np.uint64(1) << np.uint64(j % 64)
+    dt = (time.perf_counter() - t0) / flips
+    print(f"n={n}: {dt * 1e6:.1f} us per evaluate+build pair")
+    ev.close()
