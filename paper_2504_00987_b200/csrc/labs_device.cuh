@@ -47,11 +47,18 @@ template <int L, bool MT>
 struct TileSlot {
   uint64_t mt[MT ? kMtN : 1];    // raw mt19937_64 state
   uint64_t out[MT ? kMtN : PhiloxRng::kBlock];  // tempered block / Philox block
-  uint8_t tenure[MT ? kMtN : 4];  // MT: tenure table of the block (labs_rng.cuh)
-  int32_t tenure_par[4];          // MT: {min_t, range, table window, pad}
+  uint8_t tenure[MT ? kMtN : PhiloxRng::kBlock];  // tenure table of the block (labs_rng.cuh)
+  // {min_t, range, table window (MT), pad} and, for Philox, {k0, k1, s0, s1}
+  int32_t tenure_par[MT ? 4 : 8];
   TileCtl ctl;
   WalkSmemL<L> walk;
 };
+using TileSlotPh64 = TileSlot<64, false>;
+static_assert(offsetof(TileSlotPh64, tenure) - offsetof(TileSlotPh64, out) == kPhTabOff &&
+                  offsetof(TileSlotPh64, tenure_par) - offsetof(TileSlotPh64, out) == kPhParOff &&
+                  offsetof(TileSlotPh64, tenure_par) + 16 - offsetof(TileSlotPh64, out) ==
+                      kPhKeyOff,
+              "the Philox table, parameters and key must follow the block");
 using TileSlotMt64 = TileSlot<64, true>;
 static_assert(offsetof(TileSlotMt64, tenure) - offsetof(TileSlotMt64, out) == kTenOff &&
                   offsetof(TileSlotMt64, tenure_par) - offsetof(TileSlotMt64, out) == kTenParOff,
@@ -272,11 +279,10 @@ __global__ void __launch_bounds__(32 * kWarps, min_blocks<NS>()) k_tabu(WalkArgs
       mt_store(sl.mt, A.mt[item], rng.idx);
     } else {
       PhiloxRng rng;
-      rng.k0 = static_cast<uint32_t>(A.seed);
-      rng.k1 = static_cast<uint32_t>(A.seed >> 32);
-      rng.s0 = static_cast<uint32_t>(item);
-      rng.s1 = 0x4C414253u;  // "LABS"
-      rng.bind(sl.out, A.ctr_base);
+      rng.set_key(sl.out, static_cast<uint32_t>(A.seed), static_cast<uint32_t>(A.seed >> 32),
+                  0x4C414253u);  // "LABS"
+      rng.set_stream(static_cast<uint32_t>(item));
+      rng.bind(A.ctr_base);
       for (int k = 0; k < A.walks; ++k) {
         int steps = 0;
         bestE = tabu_walk<NS>(w, n, cur, rng, A.cfg, best,
@@ -314,8 +320,8 @@ struct PhiloxBind {
   uint64_t* buf;
   int64_t offset;
   __device__ __forceinline__ void load(int r, PhiloxRngT<T>& rng) {
-    rng.s0 = static_cast<uint32_t>(offset + r);
-    rng.bind(buf, ctr[r]);
+    rng.set_stream(static_cast<uint32_t>(offset + r));
+    rng.bind(ctr[r]);
   }
   __device__ __forceinline__ void save(int r, PhiloxRngT<T>& rng) {
     if (tile_lane<T>() == 0) ctr[r] = rng.ctr;
@@ -363,11 +369,10 @@ k_memetic(MemeticArgs A) {
     run_policy<NS, T>(A, w, rng, rb, sl.ctl);
   } else {
     PhiloxRngT<T> rng;
-    rng.k0 = static_cast<uint32_t>(A.base_seed);
-    rng.k1 = static_cast<uint32_t>(A.base_seed >> 32);
-    rng.s0 = 0;
-    rng.s1 = 0x4D454D45u;  // "MEME"
-    rng.bind(sl.out, 0);  // valid until a replica is loaded
+    rng.set_key(sl.out, static_cast<uint32_t>(A.base_seed),
+                static_cast<uint32_t>(A.base_seed >> 32), 0x4D454D45u);  // "MEME"
+    rng.set_stream(0);
+    rng.bind(0);  // valid until a replica is loaded
     PhiloxBind<T> rb{A.ctr, sl.out, A.replica_offset};
     run_policy<NS, T>(A, w, rng, rb, sl.ctl);
   }

@@ -340,9 +340,54 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0,
 // draws base + 2(l + T q) and base + 2(l + T q) + 1, so the 10-round cost is
 // paid once per 64 draws and spread over the tile. The stream is defined per
 // draw index d (block d >> 1, half d & 1), independent of the buffering.
+//
+// Shared layout after the 64-draw block (TileSlot, labs_device.cuh): the
+// block's tenure table (64 bytes, as the MT table: min_t + Lemire reduction
+// of each draw for the current walk's window, 0xFF where the reduction might
+// reject), its parameters {min_t, range, -, -} and the key {k0, k1, s0, s1},
+// so the generator itself is three registers (buffer, 64-bit counter) plus
+// the count of table entries still valid from the counter on.
+constexpr int kPhBlock = 64;
+constexpr uint32_t kPhTabOff = 8u * kPhBlock;
+constexpr uint32_t kPhParOff = kPhTabOff + kPhBlock;
+constexpr uint32_t kPhKeyOff = kPhParOff + 16;
+
+// Tabulate the tenure draw of block entries [lo, 64); returns the first
+// entry >= lo not served from the table (64 when all are).
 template <int T>
-__device__ __noinline__ void philox_refill(uint32_t buf, uint64_t base, uint32_t k0,
-                                           uint32_t k1, uint32_t s0, uint32_t s1) {
+__device__ __forceinline__ int philox_tenure_fill(uint32_t buf, int lo) {
+  const int min_t = lds_s32(buf + kPhParOff);
+  const uint32_t r32 = static_cast<uint32_t>(lds_s32(buf + kPhParOff + 4));
+  if (min_t + static_cast<int>(r32) - 1 > 254) return lo;
+  int first = kPhBlock;
+#pragma unroll
+  for (int q = 0; q < kPhBlock / T; ++q) {
+    const int i = tile_lane<T>() + T * q;
+    bool rej = false;
+    if (i >= lo) {
+      const uint64_t x = lds_u64(buf + 8u * static_cast<uint32_t>(i));
+      const uint64_t p0 = static_cast<uint64_t>(static_cast<uint32_t>(x)) * r32;
+      const uint64_t p1 =
+          static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * r32 + (p0 >> 32);
+      rej = static_cast<uint32_t>(p1) == 0 && static_cast<uint32_t>(p0) < r32;
+      sts_u8(buf + kPhTabOff + i, rej ? 0xFFu : static_cast<uint32_t>(min_t) +
+                                                   static_cast<uint32_t>(p1 >> 32));
+    }
+    const uint32_t b = tile_ballot<T>(rej);
+    if (b && first == kPhBlock) first = T * q + __ffs(b) - 1;
+  }
+  tile_sync<T>();
+  return first;
+}
+
+// Refill the block holding draw `base` (a multiple of 64) and tabulate its
+// tenures; returns the count of table entries valid from entry 0.
+template <int T>
+__device__ __noinline__ int philox_refill(uint32_t buf, uint64_t base) {
+  const uint32_t k0 = static_cast<uint32_t>(lds_s32(buf + kPhKeyOff));
+  const uint32_t k1 = static_cast<uint32_t>(lds_s32(buf + kPhKeyOff + 4));
+  const uint32_t s0 = static_cast<uint32_t>(lds_s32(buf + kPhKeyOff + 8));
+  const uint32_t s1 = static_cast<uint32_t>(lds_s32(buf + kPhKeyOff + 12));
 #pragma unroll
   for (int q = 0; q < 32 / T; ++q) {
     const uint32_t rel = tile_lane<T>() + T * q;
@@ -353,49 +398,98 @@ __device__ __noinline__ void philox_refill(uint32_t buf, uint64_t base, uint32_t
     sts_u64(buf + 16u * rel + 8u, static_cast<uint64_t>(c[3]) << 32 | c[2]);
   }
   tile_sync<T>();
+  return philox_tenure_fill<T>(buf, 0);
 }
 
 template <int T>
-struct PhiloxRngT {
-  static constexpr int kBlock = 64;
-  uint32_t k0, k1;   // key = seed
-  uint32_t s0, s1;   // stream (walker / replica id)
-  uint64_t ctr;      // next draw index
-  uint32_t buf_s;    // shared-window address of the current 64-draw block
+__device__ __noinline__ int philox_tenure_table(uint32_t buf, int lo, int min_t, uint32_t range) {
+  if (tile_lane<T>() == 0) {
+    sts_s32(buf + kPhParOff, min_t);
+    sts_s32(buf + kPhParOff + 4, static_cast<int32_t>(range));
+  }
+  tile_sync<T>();
+  return philox_tenure_fill<T>(buf, lo) - lo;
+}
 
-  // Bind to a shared buffer of kBlock words and fill the block holding ctr.
-  __device__ __forceinline__ void bind(uint64_t* buf, uint64_t c) {
+template <int T>
+struct PhiloxRngT;
+template <int T>
+struct PhiloxTenure {
+  int v;
+  PhiloxRngT<T> rng;
+};
+template <int T>
+__device__ __noinline__ PhiloxTenure<T> philox_tenure_slow(PhiloxRngT<T> r);
+
+template <int T>
+struct PhiloxRngT {
+  static constexpr int kBlock = kPhBlock;
+  uint32_t buf_s;  // shared-window address of the current 64-draw block
+  uint64_t ctr;    // next draw index
+  int t_rem;       // table entries valid from ctr on (<= 0: none)
+
+  // Key and stream live in shared memory next to the block (tile-uniform
+  // writes by lane 0; bind/set_stream order them before the next refill).
+  __device__ __forceinline__ void set_key(uint64_t* buf, uint32_t k0, uint32_t k1, uint32_t s1) {
     buf_s = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+    if (tile_lane<T>() == 0) {
+      sts_s32(buf_s + kPhKeyOff, static_cast<int32_t>(k0));
+      sts_s32(buf_s + kPhKeyOff + 4, static_cast<int32_t>(k1));
+      sts_s32(buf_s + kPhKeyOff + 12, static_cast<int32_t>(s1));
+      sts_s32(buf_s + kPhParOff, 0);  // tenure window {0, 1} until a walk sets one
+      sts_s32(buf_s + kPhParOff + 4, 1);
+    }
+    tile_sync<T>();
+  }
+  __device__ __forceinline__ void set_stream(uint32_t s0) {
+    if (tile_lane<T>() == 0) sts_s32(buf_s + kPhKeyOff + 8, static_cast<int32_t>(s0));
+    tile_sync<T>();
+  }
+  // Position at draw c and fill the block holding it (key and stream set).
+  __device__ __forceinline__ void bind(uint64_t c) {
     ctr = c;
-    philox_refill<T>(buf_s, ctr & ~static_cast<uint64_t>(kBlock - 1), k0, k1, s0, s1);
+    const int valid = philox_refill<T>(buf_s, ctr & ~static_cast<uint64_t>(kBlock - 1));
+    t_rem = valid - static_cast<int>(static_cast<uint32_t>(ctr) & (kBlock - 1));
   }
   __device__ __forceinline__ uint64_t next() {
     const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
-    if (off == 0) philox_refill<T>(buf_s, ctr, k0, k1, s0, s1);
+    if (off == 0) t_rem = philox_refill<T>(buf_s, ctr);
     const uint64_t v = lds_u64(buf_s + 8u * off);
     ++ctr;
+    --t_rem;
     return v;
   }
   __device__ __forceinline__ int room() {
     const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
-    if (off == 0) philox_refill<T>(buf_s, ctr, k0, k1, s0, s1);
+    if (off == 0) t_rem = philox_refill<T>(buf_s, ctr);
     return kBlock - static_cast<int>(off);
   }
   __device__ __forceinline__ uint64_t peek_lane(int i) const {
     return lds_u64(buf_s + 8u * ((static_cast<uint32_t>(ctr) & (kBlock - 1)) + i));
   }
   __device__ __forceinline__ void advance(int count) {
-    const uint64_t nc = ctr + static_cast<uint64_t>(count);
     // crossing into a new block mid-way is impossible: count <= room()
-    ctr = nc;
+    ctr += static_cast<uint64_t>(count);
+    t_rem -= count;
   }
-  int tmin;        // the walk's tenure window (begin_walk)
-  uint32_t trange;
+  // A walk's tenure window: tabulate the rest of the current block for it
+  // (a block not yet filled is tabulated by its refill).
   __device__ __forceinline__ void begin_walk(int min_t, uint32_t range, int /*steps*/) {
-    tmin = min_t;
-    trange = range;
+    const int off = static_cast<int>(static_cast<uint32_t>(ctr) & (kBlock - 1));
+    t_rem = philox_tenure_table<T>(buf_s, off == 0 ? kBlock : off, min_t, range);
   }
-  __device__ __forceinline__ int tenure();
+  __device__ __forceinline__ int tenure() {
+    if (t_rem > 0) {
+      const uint32_t off = static_cast<uint32_t>(ctr) & (kBlock - 1);
+      const int v = static_cast<int>(lds_u8(buf_s + kPhTabOff + off));
+      ++ctr;
+      --t_rem;
+      return v;
+    }
+    const PhiloxTenure<T> p = philox_tenure_slow<T>(*this);
+    *this = p.rng;
+    return p.v;
+  }
 };
 using PhiloxRng = PhiloxRngT<32>;
 
@@ -506,9 +600,26 @@ __device__ __forceinline__ int uniform_below(R& rng, uint32_t r32) {
   return static_cast<int>(p1 >> 32);
 }
 
+// Tenure outside the table: at a block start refill (which tabulates the
+// block); a possibly-rejecting entry takes the full uniform_int, after which
+// the rest of the block is re-tabulated.
 template <int T>
-__device__ __forceinline__ int PhiloxRngT<T>::tenure() {
-  return tmin + uniform_below(*this, trange);
+__device__ __noinline__ PhiloxTenure<T> philox_tenure_slow(PhiloxRngT<T> r) {
+  uint32_t off = static_cast<uint32_t>(r.ctr) & (kPhBlock - 1);
+  if (off == 0) r.t_rem = philox_refill<T>(r.buf_s, r.ctr);
+  if (r.t_rem > 0) {
+    const int v = static_cast<int>(lds_u8(r.buf_s + kPhTabOff + off));
+    ++r.ctr;
+    --r.t_rem;
+    return {v, r};
+  }
+  const int min_t = lds_s32(r.buf_s + kPhParOff);
+  const uint32_t range = static_cast<uint32_t>(lds_s32(r.buf_s + kPhParOff + 4));
+  const int v = min_t + uniform_below(r, range);
+  off = static_cast<uint32_t>(r.ctr) & (kPhBlock - 1);
+  r.t_rem = off == 0 ? 0 : philox_tenure_fill<T>(r.buf_s, static_cast<int>(off)) -
+                               static_cast<int>(off);
+  return {v, r};
 }
 
 // Outside the tabulated window: at the block end twist (which tabulates the
