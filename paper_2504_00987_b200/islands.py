@@ -94,6 +94,8 @@ class Islands:
             for p in self.peer_ptrs:
                 self.solver.ctx.ipc_close(p)
             self.peer_ptrs = []
+            if self.world > 1:
+                dist.barrier(group=self.group)  # every mapping closed before any flag is freed
 
     def _allreduce(self, values, op):
         t = torch.tensor(values, dtype=torch.int64, device=self.comm_device)
