@@ -349,6 +349,17 @@ int labs_exhaustive_optimum(labs_ctx* ctx, int n, int64_t* optimal_energy,
                             uint64_t* witnesses, int64_t cap, int64_t* count);
 int labs_local_optima(labs_ctx* ctx, int n, int64_t* count);
 
+/* ------------------------------------------ K6: skew-symmetry deviation - */
+/* Replaces deviation / deviation_with_edits (proj/include/labsolve/
+ * skew.hpp:21-40; skew.cpp:110-187) on the device: every pair-count
+ * evaluation of the reference's loop order runs in its own thread, and the
+ * reference's early exit (right after the first zero) and budget charging
+ * are recovered exactly, so value, budget_exceeded and evaluations equal
+ * the reference's. budget = 0: unlimited. 3 <= n <= LABS_MAX_N. */
+int labs_skew_deviation(labs_ctx* ctx, int n, const uint64_t* words, int with_edits,
+                        uint64_t budget, int32_t* value, int32_t* budget_exceeded,
+                        uint64_t* evaluations);
+
 /* ------------------------------------------------------- diagnostics --- */
 /* Measured INT32 lane-instruction rate of this device (IMAD on the FMA pipe
  * alongside IADD3/LOP3 on the ALU pipe), in Gop/s: the issue ceiling of

@@ -50,7 +50,7 @@ EXPORTS = [
     "labs_solver_population", "labs_solver_state_size", "labs_solver_save", "labs_solver_load",
     "labs_solver_stop_flag", "labs_solver_set_peer_stops", "labs_ipc_export", "labs_ipc_open",
     "labs_ipc_close", "labs_run_replicas_multi", "labs_bench_imad_peak",
-    "labs_eval_create", "labs_eval_destroy", "labs_eval_run",
+    "labs_eval_create", "labs_eval_destroy", "labs_eval_run", "labs_skew_deviation",
 ]
 CROSSOVER_UNIFORM = 0
 CROSSOVER_ONE_POINT = 1
@@ -190,6 +190,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.labs_eval_create.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
     L.labs_eval_destroy.argtypes = [C.c_void_p]
     L.labs_eval_run.argtypes = [C.c_void_p, u64p, i32p, i64p, i64p]
+    L.labs_skew_deviation.argtypes = [C.c_void_p, C.c_int, u64p, C.c_int, C.c_uint64, i32p,
+                                      i32p, u64p]
     L.labs_exhaustive_optimum.argtypes = [C.c_void_p, C.c_int, i64p, u64p, C.c_int64, i64p]
     L.labs_local_optima.argtypes = [C.c_void_p, C.c_int, i64p]
     L.labs_solver_population.argtypes = [C.c_void_p, u64p, i32p]
@@ -330,6 +332,16 @@ class Context:
         g = C.c_double(0)
         _check(self.L.labs_bench_imad_peak(self.h, C.byref(g)))
         return float(g.value)
+
+    # -- K6 ---------------------------------------------------------------
+    def skew_deviation(self, n: int, words, with_edits: bool = False, budget: int = 0):
+        """(value, budget_exceeded, evaluations) of deviation[_with_edits]."""
+        w = _words(words, n)
+        v, ex, ev = C.c_int32(0), C.c_int32(0), C.c_uint64(0)
+        _check(self.L.labs_skew_deviation(self.h, n, _ptr(w, u64p), 1 if with_edits else 0,
+                                          C.c_uint64(budget), C.byref(v), C.byref(ex),
+                                          C.byref(ev)))
+        return int(v.value), bool(ex.value), int(ev.value)
 
     # -- K1 ---------------------------------------------------------------
     def build_state(self, n: int, words, neighbors: bool = True):

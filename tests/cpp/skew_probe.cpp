@@ -1,4 +1,4 @@
-// Host-only probe of the skew.hpp drop-in for tests/test_skew_cpu.py:
+// Probe of the skew.hpp drop-in (device deviation) for tests/test_skew_gpu.py:
 // stdin lines "n budget edits w0 [w1 ...]" -> "value exceeded evaluations".
 #include <cstdint>
 #include <iostream>

@@ -1,23 +1,11 @@
-"""skew.hpp drop-in (deviation from skew-symmetry, host analysis) against the
-reference's own deviation / deviation_with_edits, including budgets and
-evaluation counts, and the Table II d(S) column."""
+"""skew.hpp drop-in: the Table II d(S) column of the golden vectors and the
+host Rng. The deviation search itself runs on the device (K6) and is checked
+against the reference's deviation / deviation_with_edits — values, budgets
+and evaluation counts — in tests/test_skew_gpu.py."""
 import os
 import subprocess
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
-
-
-def test_deviation_matches_reference(golden):
-    exe = os.path.join(ROOT, "tests", "cpp", "skew_probe")
-    assert os.path.exists(exe), "build with __graft_entry__.build()"
-    cases = golden["skew"]
-    stdin = "\n".join(f'{c["n"]} {c["budget"]} {int(c["edits"])} ' +
-                      " ".join(str(w) for w in c["words"]) for c in cases) + "\n"
-    r = subprocess.run([exe], input=stdin, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr
-    got = [tuple(int(x) for x in line.split()) for line in r.stdout.splitlines()]
-    want = [(c["value"], int(c["budget_exceeded"]), c["evaluations"]) for c in cases]
-    assert got == want
 
 
 def test_table_deviation_column(golden):
