@@ -518,6 +518,14 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
       do {
         step(std::integral_constant<int, 0>{});
       } while (!walk_ended());
+    } else if constexpr (LABS_SINGLE_C && kUnroll) {
+      // one C buffer, unrolled by two: no parity to carry between walks
+      while (true) {
+        step(std::integral_constant<int, 0>{});
+        if (walk_ended()) break;
+        step(std::integral_constant<int, 1>{});
+        if (walk_ended()) break;
+      }
     } else if constexpr (kUnroll) {
       if (par) goto odd;
       while (true) {
