@@ -6,10 +6,11 @@
 // evaluation. Here every evaluation of the reference's order is indexed
 // (rotation-major, exactly as its nested loops visit them) and computed by
 // its own thread; the sequential semantics are then recovered exactly:
-//   P = min(first zero index + 1, budget (if any), total)
-//   value = min over evaluations [0, P)     evaluations = P
-//   budget_exceeded = budget < total and no zero before index budget
-// (a zero at index budget-1 ends the loops without another charge).
+//   want = first zero index + 1 (+1 where the reference's loop has no exit
+//          test between two evaluations), or all evaluations
+//   P = min(want, budget (if any));  value = min over [0, P); evaluations = P
+//   budget_exceeded = budget < want (a charge was attempted past the budget;
+//   a zero at index budget-1 ends the loops without another charge).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -145,8 +146,19 @@ extern "C" int labs_skew_deviation(labs_ctx* ctx, int n, const uint64_t* words, 
   unsigned long long zero = 0;
   LABS_D2H(&zero, dz.p, sizeof(zero));
   LABS_CUDA(cudaStreamSynchronize(ctx->stream));
-  uint64_t prefix = total;
-  if (zero != ~0ull && zero + 1 < prefix) prefix = zero + 1;
+  // Evaluations the reference's loops want: up to the first zero, except
+  // that its insertion loop of even lengths with edits has no early-exit
+  // test between the two spins (skew.cpp:172-179), so a zero at spin +1
+  // still charges and evaluates spin -1.
+  uint64_t want = total;
+  if (zero != ~0ull) {
+    want = zero + 1;
+    if (mode == kEditEven) {
+      const uint64_t k = zero % per_rotation(mode, n);
+      if (k >= static_cast<uint64_t>(n) && ((k - n) & 1) == 0) want += 1;
+    }
+  }
+  uint64_t prefix = want;
   if (budget && budget < prefix) prefix = budget;
   int m = INT_MAX;
   if (prefix) {
@@ -157,6 +169,6 @@ extern "C" int labs_skew_deviation(labs_ctx* ctx, int n, const uint64_t* words, 
   }
   *value = prefix ? m : -1;
   *evaluations = prefix;
-  *budget_exceeded = (budget && budget < total && (zero == ~0ull || zero >= budget)) ? 1 : 0;
+  *budget_exceeded = (budget && budget < want) ? 1 : 0;  // a charge past the budget
   return LABS_OK;
 }
