@@ -137,9 +137,9 @@ extern "C" int labs_skew_deviation(labs_ctx* ctx, int n, const uint64_t* words, 
   LABS_CUDA(cudaMemsetAsync(dz.p, 0xff, sizeof(unsigned long long), ctx->stream));
   const int big = INT_MAX;
   LABS_H2D(dm.p, &big, sizeof(int));
-  const uint64_t want = (total + 255) / 256;
+  const uint64_t blocks = (total + 255) / 256;
   const unsigned grid = static_cast<unsigned>(
-      want < static_cast<uint64_t>(ctx->sm_count) * 16 ? want : ctx->sm_count * 16);
+      blocks < static_cast<uint64_t>(ctx->sm_count) * 16 ? blocks : ctx->sm_count * 16);
   k_skew_eval<<<grid, 256, 0, ctx->stream>>>(n, mode, dw.as<uint64_t>(), total,
                                              dv.as<uint8_t>(), dz.as<unsigned long long>());
   LABS_CUDA(cudaGetLastError());
