@@ -562,11 +562,17 @@ struct Walker {
     const int j = T * B + o.ln;
     const bool isp = j == o.pos;
     const int wv = v[B].s1 + o.nsig * (v[B].cg + v[B].cg + v[B].qg);
-    // D += delta, or the flip's -D (2p - D keyed) as an increment, so D
-    // stays in its register (no select into a temporary and copy back)
-    const int delta = MS[B] * wv + (o.nsig * v[B].s2 - 32 * Sc::kD);
-    const int flip = Sc::kKeyed ? 2 * o.pos - D[B] - D[B] : -D[B] - D[B];
-    D[B] += isp ? flip : delta;
+    if constexpr (NS >= 3) {
+      // D += delta, or the flip's -D (2p - D keyed) as an increment, so D
+      // stays in its register (no select into a temporary and copy back):
+      // +3 % at n = 119, -0.3 % at n = 64 (measured), hence NS >= 3 only
+      const int delta = MS[B] * wv + (o.nsig * v[B].s2 - 32 * Sc::kD);
+      const int flip = Sc::kKeyed ? 2 * o.pos - D[B] - D[B] : -D[B] - D[B];
+      D[B] += isp ? flip : delta;
+    } else {
+      const int dn = D[B] + o.nsig * v[B].s2 + MS[B] * wv - 32 * Sc::kD;
+      D[B] = isp ? (Sc::kKeyed ? 2 * o.pos - D[B] : -D[B]) : dn;
+    }
     if (!isp) sts_s32_off<kQOff + 4 * T * B>(o.a6, v[B].qg + o.c32 * MS[B]);
     CK[B] += o.nsig * (v[B].smv + v[B].spv);
     sts_s32_off<kBufW<CB> + kCOff + 4 * T * B>(o.aW, CK[B]);
