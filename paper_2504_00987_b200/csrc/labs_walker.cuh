@@ -75,6 +75,9 @@ namespace labsk {
 #ifndef LABS_ADDR_ASM
 #define LABS_ADDR_ASM 1
 #endif
+#ifndef LABS_CHECKED
+#define LABS_CHECKED 0
+#endif
 // Compile-time loop: f(std::integral_constant<int, i>) for i in [0, N).
 template <int N, int I = 0, class F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -546,6 +549,45 @@ struct Walker {
   static constexpr int kCOff = kS4 ? 4 * L - (int)offsetof(Smem, S4) - 4 * SO : 0;
   static constexpr int kQOff = kS4 ? (int)offsetof(Smem, Q) - (int)offsetof(Smem, S4) - 4 * SO : 0;
 
+#if LABS_CHECKED
+  // Checked builds (-DLABS_CHECKED=1; compute-sanitizer is unavailable on
+  // this pool): every gather/store address of the step must fall inside its
+  // own array, and a spin read outside [0, n) must hit the zero padding.
+  __device__ uint32_t smem_base() const {
+    return aS0 - static_cast<uint32_t>(reinterpret_cast<const char*>(sm->spins() + SO) -
+                                       reinterpret_cast<const char*>(sm));
+  }
+  __device__ void check_addr(uint32_t a, int bytes, int array, int line) const {
+    const uint32_t base = smem_base();
+    uint32_t lo, hi;
+    if (array == 0) {  // C mirror
+      lo = base + static_cast<uint32_t>(offsetof(Smem, C2));
+      hi = lo + sizeof(sm->C2);
+    } else if (array == 1) {  // Q
+      lo = base + static_cast<uint32_t>(offsetof(Smem, Q));
+      hi = lo + sizeof(sm->Q);
+    } else {  // spins
+      lo = base + static_cast<uint32_t>(reinterpret_cast<const char*>(sm->spins()) -
+                                        reinterpret_cast<const char*>(sm));
+      hi = lo + static_cast<uint32_t>(kE * (3 * L + 8));
+    }
+    if (a < lo || a + bytes > hi) {
+      printf("LABS_CHECKED line %d: lane %d address %u outside array %d [%u, %u)\n", line,
+             tile_lane<T>(), a, array, lo, hi);
+      __trap();
+    }
+  }
+  __device__ void check_spin(uint32_t a, int v, int line) const {
+    check_addr(a, kE, 2, line);
+    const int x = static_cast<int>(a - aS0) / kE;  // logical position
+    if ((x < 0 || x >= n) && v != 0) {
+      printf("LABS_CHECKED line %d: spin read at position %d (n = %d) is %d, not padding\n",
+             line, x, n, v);
+      __trap();
+    }
+  }
+#endif
+
   template <int CB, int B>
   __device__ __forceinline__ void slot_load(const StepOps& o, SlotIn (&v)[NS]) {
     constexpr int e = kE;
@@ -555,6 +597,14 @@ struct Walker {
     v[B].s2 = lds_spin<e, 2 * e * T * B>(o.a4);                  // kSpin s_{2j-p}
     v[B].smv = lds_spin<e, -e * T * B>(o.a2);                    // kSpin s_{p-j}
     v[B].spv = lds_spin<e, e * T * B>(o.a3);                     // kSpin s_{p+j}
+#if LABS_CHECKED
+    check_addr(o.a5 + kBufC<CB> + kCOff + 4 * T * B, 4, 0, __LINE__);
+    check_addr(o.a6 + kQOff + 4 * T * B, 4, 1, __LINE__);
+    check_spin(o.a1 - e * T * B, v[B].s1, __LINE__);
+    check_spin(o.a4 + 2 * e * T * B, v[B].s2, __LINE__);
+    check_spin(o.a2 - e * T * B, v[B].smv, __LINE__);
+    check_spin(o.a3 + e * T * B, v[B].spv, __LINE__);
+#endif
     if constexpr (B + 1 < NS) slot_load<CB, B + 1>(o, v);
   }
   template <int CB, int B>
@@ -573,6 +623,10 @@ struct Walker {
       const int dn = D[B] + o.nsig * v[B].s2 + MS[B] * wv - 32 * Sc::kD;
       D[B] = isp ? (Sc::kKeyed ? 2 * o.pos - D[B] : -D[B]) : dn;
     }
+#if LABS_CHECKED
+    check_addr(o.aW + kBufW<CB> + kCOff + 4 * T * B, 4, 0, __LINE__);
+    check_addr(o.aWm + kBufW<CB> + kCOff - 4 * T * B, 4, 0, __LINE__);
+#endif
     if (!isp) sts_s32_off<kQOff + 4 * T * B>(o.a6, v[B].qg + o.c32 * MS[B]);
     CK[B] += o.nsig * (v[B].smv + v[B].spv);
     sts_s32_off<kBufW<CB> + kCOff + 4 * T * B>(o.aW, CK[B]);
@@ -591,6 +645,14 @@ struct Walker {
     const uint32_t up = static_cast<uint32_t>(pos);
     const uint32_t a_sig = aS0 + e * up;
     const int sig16 = lds_spin<e, 0>(a_sig);
+#if LABS_CHECKED
+    check_addr(pend_a, e, 2, __LINE__);
+    check_addr(a_sig, e, 2, __LINE__);
+    if (pos < 0 || pos >= n || sig16 == 0) {
+      printf("LABS_CHECKED: flip position %d (n = %d) with spin %d\n", pos, n, sig16);
+      __trap();
+    }
+#endif
     const int sig = sig16 >> Sc::kSpinShift;
     StepOps o;
     o.nsig = -sig;
