@@ -47,6 +47,15 @@ RunResult run_replicas(const ParallelConfig& cfg, ReplicaReport* report) {
                                     per.data(), traces ? recs.data() : nullptr, cap,
                                     traces ? lens.data() : nullptr));
   for (int r = 0; traces && r < cfg.replicas; ++r) detail::check_trace_len(lens[r], cap);
+  if (!cfg.run_threaded) {
+    // The reference's sequential loop publishes in replica order
+    // (parallel.cpp:49-50), so a tie goes to the lowest replica index; the
+    // device's first-publisher rule is the threaded run's.
+    int win = 0;
+    for (int r = 1; r < cfg.replicas; ++r)
+      if (per[r].best_energy < per[win].best_energy) win = r;
+    best = per[win];
+  }
   auto convert = [&](const labs_run_result& o) {
     RunResult r;
     r.best = Sequence(cfg.n);

@@ -244,6 +244,24 @@ static void parallel() {
   CHECK(res.reached_target && res.best_energy == 24 && naive_energy(res.best) == 24);
   CHECK(res.seed == race.base_seed + static_cast<std::uint64_t>(res.replica_id));
   CHECK(report.results.size() == 6 && report.traces.size() == 6);
+  // Sequential mode: replicas publish in index order in the reference, so a
+  // tie goes to the lowest index, on every run (n = 36, seeds 321.., five
+  // memetic iterations: replicas 2 and 6 tie at E = 118).
+  ParallelConfig seq;
+  seq.n = 36;
+  seq.replicas = 7;
+  seq.base_seed = 321;
+  seq.run_threaded = false;
+  seq.memetic.target_energy = 0;
+  seq.memetic.max_iterations = 5;
+  for (int rep = 0; rep < 5; ++rep) {
+    ReplicaReport all;
+    RunResult w = run_replicas(seq, &all);
+    int first = 0;
+    for (int r = 1; r < seq.replicas; ++r)
+      if (all.results[r].best_energy < all.results[first].best_energy) first = r;
+    CHECK(w.replica_id == first && w.best_energy == all.results[first].best_energy);
+  }
   ParallelConfig broken;
   broken.n = 12;
   broken.replicas = 3;

@@ -243,7 +243,12 @@ def test_run_replicas_multi_matches_single_gpu(ctx, oracle):
         assert per[r]["trace"] == per1[r]["trace"]
     assert best["best_energy"] == min(x["best_energy"] for x in per)
     one, _ = capi.run_replicas_multi([ctx], n, R, base, p)
-    assert (one["best_energy"], one["replica_id"]) == (b1["best_energy"], b1["replica_id"])
+    # Ties go to the first publisher, which is completion order on the device
+    # (as in the reference's threaded run), so two runs may pick different
+    # members of the tie.
+    ties = {r for r in range(R) if per[r]["best_energy"] == best["best_energy"]}
+    assert one["best_energy"] == b1["best_energy"] == best["best_energy"]
+    assert {one["replica_id"], b1["replica_id"], best["replica_id"]} <= ties
     with pytest.raises(ValueError):
         capi.run_replicas_multi([], n, R, base, p)
     ctx2.close()
