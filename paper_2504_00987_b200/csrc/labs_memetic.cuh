@@ -235,8 +235,8 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
   constexpr int NC = (T * NS) / 32;
   // Unrolled by two for short walkers (the two bodies keep different
   // register assignments, which saves moves); one body from NS = 3 on, where
-  // two copies of the longer step body miss the L0 instruction cache
-  // (measured: +0.8% / -3.4% at n = 64 / 119 unrolled vs one body).
+  // the longer step body gains nothing from a second copy (final build:
+  // -1.4% / +1.3% / +0.6% at n = 80 / 96 / 119 unrolled).
   constexpr bool kUnroll = T == 32 ? (LABS_UNROLL_T32 && NS <= LABS_UNROLL_MAX_NS)
                                    : LABS_UNROLL_T16;
   const int ln = tile_lane<T>();
