@@ -21,6 +21,9 @@
 #ifndef LABS_UNROLL_MAX_NS
 #define LABS_UNROLL_MAX_NS 2
 #endif
+#ifndef LABS_UNROLL_EXTRA_NS  // one more walker width that is unrolled
+#define LABS_UNROLL_EXTRA_NS 4
+#endif
 #ifndef LABS_UNROLL_T16
 #define LABS_UNROLL_T16 0
 #endif
@@ -234,11 +237,12 @@ __device__ __forceinline__ void memetic_tiles(const MemeticArgs& A, Walker<NS, T
                                               R& rng, RB& rb, TileCtl& ctl) {
   constexpr int NC = (T * NS) / 32;
   // Unrolled by two for short walkers (the two bodies keep different
-  // register assignments, which saves moves); one body from NS = 3 on, where
-  // the longer step body gains nothing from a second copy (final build:
-  // -1.4% / +1.3% / +0.6% at n = 80 / 96 / 119 unrolled).
-  constexpr bool kUnroll = T == 32 ? (LABS_UNROLL_T32 && NS <= LABS_UNROLL_MAX_NS)
-                                   : LABS_UNROLL_T16;
+  // register assignments, which saves moves), and at NS = 4 (+0.6% at
+  // n = 119); one body at NS = 3 (-1.4% / +1.3% at n = 80 / 96 unrolled) and
+  // from NS = 5 on.
+  constexpr bool kUnroll =
+      T == 32 ? (LABS_UNROLL_T32 && (NS <= LABS_UNROLL_MAX_NS || NS == LABS_UNROLL_EXTRA_NS))
+              : LABS_UNROLL_T16;
   const int ln = tile_lane<T>();
   const int n = A.n, nw = A.nw, K = A.K;
   const int G = gridDim.x * (blockDim.x / T);  // tiles in the grid
